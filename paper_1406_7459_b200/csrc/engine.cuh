@@ -1,0 +1,174 @@
+// Host side of the B200 engine: one Engine<T> per mfd_ctx.  Owns every device
+// buffer, the CUDA stream, the cached CUDA graphs of K-step chunks, and the
+// reference-semantics loop control of Simulation<T>::step / dynamics::relax
+// (sim.hpp:33-62, dynamics.hpp:157-198).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mfd.h"
+#include "step_kernels.cuh"
+#include "tensor_api.h"
+
+namespace mfd {
+
+struct Error : std::runtime_error {
+    mfd_status code;
+    Error(mfd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(MFD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kMu0 = 4.0e-7 * kPi;                       // constants.hpp:9
+constexpr double kRadToDegPerNs = 180.0 / kPi * 1e-9;       // dynamics.hpp:34
+constexpr int kMaxL = 2048;
+
+inline int next_pow2(int n) { int p = 1; while (p < n) p <<= 1; return p; }
+inline int padded_size(int n) { return next_pow2(2 * n); }  // demag.hpp:24
+
+// Calls f.template operator()<L>() for the power of two L (1..kMaxL).
+template <class F>
+void with_pow2(int L, F&& f) {
+    switch (L) {
+        case 1: f.template operator()<1>(); break;
+        case 2: f.template operator()<2>(); break;
+        case 4: f.template operator()<4>(); break;
+        case 8: f.template operator()<8>(); break;
+        case 16: f.template operator()<16>(); break;
+        case 32: f.template operator()<32>(); break;
+        case 64: f.template operator()<64>(); break;
+        case 128: f.template operator()<128>(); break;
+        case 256: f.template operator()<256>(); break;
+        case 512: f.template operator()<512>(); break;
+        case 1024: f.template operator()<1024>(); break;
+        case 2048: f.template operator()<2048>(); break;
+        default: throw Error(MFD_EINVAL, "magfd-b200: unsupported FFT length " + std::to_string(L));
+    }
+}
+
+template <class T> __global__ void k_ybuf(int Py, int Hy, int* out);
+
+// One iteration of the per-step pipeline as enqueued in a graph.
+struct Iter {
+    int update = 1;
+    int renorm = 1;
+    int write_h = 0;
+    int sums = 0;        // accumulate sample sums into sums slot `slot`
+    int check_prev = 0;  // relax: skip if the previous slot converged
+    int slot = 0;        // torque / sums slot within the chunk
+    bool operator<(const Iter& o) const {
+        return std::tie(update, renorm, write_h, sums, check_prev, slot) <
+               std::tie(o.update, o.renorm, o.write_h, o.sums, o.check_prev, o.slot);
+    }
+};
+
+class EngineBase {
+public:
+    virtual ~EngineBase() = default;
+    virtual void set_m(const double*, const double*, const double*) = 0;
+    virtual void set_m32(const float*, const float*, const float*) = 0;
+    virtual void get_m(double*, double*, double*) = 0;
+    virtual void get_m32(float*, float*, float*) = 0;
+    virtual void set_uniform(const double dir[3]) = 0;
+    virtual void field(int which, double*, double*, double*) = 0;
+    virtual void step(long n, double* last, double* all) = 0;
+    virtual void step_async(long n) = 0;
+    virtual void sync() = 0;
+    virtual bool relax(mfd_sample_cb cb, void* user) = 0;
+    virtual mfd_sample sample_now() = 0;
+    virtual void timing(double ms[7]) = 0;
+    virtual void set_octant(const double*) = 0;
+    virtual void get_octant(double*) = 0;
+    virtual void get_spectrum(double*) = 0;
+    virtual void* state_ptr() = 0;
+    virtual cudaStream_t stream() const = 0;
+    virtual int launches_per_step() const = 0;
+    virtual double model_bytes() const = 0;
+    double t = 0;
+    long stepno = 0;
+    long long ncell = 0;
+    int precision = 64;
+};
+
+template <class T>
+class Engine final : public EngineBase {
+public:
+    Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st, int device);
+    ~Engine() override;
+
+    void set_m(const double* x, const double* y, const double* z) override;
+    void set_m32(const float* x, const float* y, const float* z) override;
+    void get_m(double* x, double* y, double* z) override;
+    void get_m32(float* x, float* y, float* z) override;
+    void set_uniform(const double dir[3]) override;
+    void field(int which, double* x, double* y, double* z) override;
+    void step(long n, double* last, double* all) override;
+    void step_async(long n) override;
+    void sync() override;
+    bool relax(mfd_sample_cb cb, void* user) override;
+    mfd_sample sample_now() override;
+    void timing(double ms[7]) override;
+    void set_octant(const double* oct) override;
+    void get_octant(double* oct) override;
+    void get_spectrum(double* out) override;
+    void* state_ptr() override { return M_[cur_]; }
+    cudaStream_t stream() const override { return stream_; }
+    int launches_per_step() const override { return terms_.demag ? 5 : 1; }
+    double model_bytes() const override;
+
+private:
+    void build_tensor_from_octant();
+    void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr);
+    void run_chunk(const std::vector<Iter>& its, int cur);
+    void fetch_chunk(int n, std::vector<double>& torque, int& err);
+    double torque_of(unsigned long long bits) const;
+    mfd_sample make_sample(const double sums[8], double torque) const;
+    void eval(int write_h, bool sums, double& torque, double sum_out[8]);
+    void check_error_after(int n_done_on_error);
+
+    mfd_grid grid_;
+    mfd_material mat_;
+    mfd_terms terms_;
+    mfd_stepper st_;
+    int device_;
+    Geo geo_{};
+    LocalParams<T> lp_{};
+    T scale_{};
+    int Py_ = 2, Pz_ = 2, Hy_ = 2, Hz_ = 2;
+
+    cudaStream_t stream_ = nullptr;
+    T* M_[2] = {nullptr, nullptr};
+    int cur_ = 0;
+    T* H_ = nullptr;                     // H_eff / H_demag output
+    C2<T>* A_ = nullptr;
+    C2<T>* B_ = nullptr;
+    T* Kt_ = nullptr;
+    C2<T>* tw_ = nullptr;
+    int* ybuf_ = nullptr;
+    double* oct_ = nullptr;              // fp64 tensor octant [6][nz][ny][nx]
+    int* err_ = nullptr;
+    unsigned long long* torque_ = nullptr;
+    double* sums_ = nullptr;             // [kMaxChunk][8]
+    double* partials_ = nullptr;
+    unsigned int* ticket_ = nullptr;
+    unsigned long long* h_torque_ = nullptr;   // pinned
+    double* h_sums_ = nullptr;                 // pinned
+    int* h_err_ = nullptr;                     // pinned
+    T* h_stage_ = nullptr;                     // pinned 3N staging
+    long long k5_blocks_ = 1;
+    static constexpr int kMaxChunk = 256;
+
+    std::map<std::pair<std::vector<Iter>, int>, cudaGraphExec_t> graphs_;
+};
+
+} // namespace mfd

@@ -1,0 +1,611 @@
+// Engine<T> method definitions; included once per precision by engine_f32.cu /
+// engine_f64.cu (explicit instantiation keeps the two builds parallel).
+#pragma once
+#include <algorithm>
+
+#include "engine.cuh"
+
+namespace mfd {
+
+template <class T>
+__global__ void k_ybuf(int Py, int Hy, int* out) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= Hy) return;
+    // dispatch on Py inside the kernel (setup only)
+    int r = 0;
+    switch (Py) {
+#define YB(L) case L: r = bufpos<T, L>(v); break;
+        YB(2) YB(4) YB(8) YB(16) YB(32) YB(64) YB(128) YB(256) YB(512) YB(1024) YB(2048)
+#undef YB
+        default: r = -1;
+    }
+    out[v] = r;
+}
+
+template <class T>
+__global__ void k_fill3(T* m, long long n, T x, T y, T z) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    m[i] = x;
+    m[i + n] = y;
+    m[i + 2 * n] = z;
+}
+
+template <class T>
+static void set_smem(const void* fn, int bytes) {
+    if (bytes > 48 * 1024)
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+}
+
+template <class T>
+Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st,
+                  int device)
+    : grid_(g), mat_(m), terms_(te), st_(st), device_(device) {
+    precision = sizeof(T) == 4 ? 32 : 64;
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+    const int Px = padded_size(g.nx);
+    Py_ = padded_size(g.ny);
+    Pz_ = padded_size(g.nz);
+    if (Px / 2 > kMaxL || Py_ > kMaxL || Pz_ > kMaxL)
+        throw Error(MFD_EINVAL, "magfd-b200: padded FFT size exceeds the engine limit (nx <= 2048, ny,nz <= 1024)");
+    geo_.nx = g.nx; geo_.ny = g.ny; geo_.nz = g.nz;
+    geo_.Px = Px; geo_.Py = Py_; geo_.Pz = Pz_;
+    geo_.N = Px / 2;
+    geo_.Hx = geo_.N + 1;
+    geo_.Hp = (geo_.Hx + 15) / 16 * 16;
+    geo_.ncell = (long long)g.nx * g.ny * g.nz;
+    ncell = geo_.ncell;
+    Hy_ = Py_ / 2 + 1;
+    Hz_ = Pz_ / 2 + 1;
+    scale_ = static_cast<T>(1.0 / ((double)Px * Py_ * Pz_));   // plan.normalization() (fft.hpp:261)
+
+    // Local-term coefficients, double then cast to T as the reference does.
+    const double Ms = m.Ms;
+    const double base = 2.0 * m.A / (kMu0 * Ms * Ms);
+    lp_.cx = static_cast<T>(base / (g.dx * g.dx));   // fields.hpp:25-27
+    lp_.cy = static_cast<T>(base / (g.dy * g.dy));
+    lp_.cz = static_cast<T>(base / (g.dz * g.dz));
+    lp_.exch = te.exchange && m.A > 0;                // fields.hpp:239
+    lp_.anis = te.anisotropy && m.Ku != 0;            // fields.hpp:241
+    lp_.ca = static_cast<T>(2.0 * m.Ku / (kMu0 * Ms * Ms));
+    lp_.ax = static_cast<T>(m.easy_axis[0]);
+    lp_.ay = static_cast<T>(m.easy_axis[1]);
+    lp_.az = static_cast<T>(m.easy_axis[2]);
+    lp_.hx = static_cast<T>(te.h_ext[0]);
+    lp_.hy = static_cast<T>(te.h_ext[1]);
+    lp_.hz = static_cast<T>(te.h_ext[2]);
+    lp_.zee = te.zeeman && (lp_.hx != 0 || lp_.hy != 0 || lp_.hz != 0);   // fields.hpp:243-245
+    const double a2 = 1.0 + m.alpha * m.alpha;
+    lp_.precess = static_cast<T>(-m.gamma / a2);                            // dynamics.hpp:54-57
+    lp_.damp = static_cast<T>(-m.alpha * m.gamma / (a2 * Ms));
+    lp_.mu0 = static_cast<T>(kMu0);
+    lp_.dt = static_cast<T>(st.dt);
+    lp_.Ms = static_cast<T>(Ms);
+    lp_.dA = m.A; lp_.dMs = Ms; lp_.dKu = m.Ku; lp_.dV = g.dx * g.dy * g.dz;
+    lp_.dax = m.easy_axis[0]; lp_.day = m.easy_axis[1]; lp_.daz = m.easy_axis[2];
+    lp_.dhx = te.h_ext[0]; lp_.dhy = te.h_ext[1]; lp_.dhz = te.h_ext[2];
+    lp_.wx = 1.0 / (g.dx * g.dx); lp_.wy = 1.0 / (g.dy * g.dy); lp_.wz = 1.0 / (g.dz * g.dz);
+
+    const long long n = geo_.ncell;
+    auto alloc = [&](auto** p, size_t bytes) { ck(cudaMalloc((void**)p, bytes ? bytes : 16), "cudaMalloc"); };
+    alloc(&M_[0], 3 * n * sizeof(T));
+    alloc(&M_[1], 3 * n * sizeof(T));
+    alloc(&H_, 3 * n * sizeof(T));
+    alloc(&err_, sizeof(int));
+    alloc(&torque_, kMaxChunk * sizeof(unsigned long long));
+    alloc(&sums_, kMaxChunk * 8 * sizeof(double));
+    alloc(&ticket_, sizeof(unsigned int));
+    ck(cudaMemset(err_, 0, sizeof(int)), "memset");
+    ck(cudaMemset(ticket_, 0, sizeof(unsigned int)), "memset");
+    ck(cudaMemset(M_[0], 0, 3 * n * sizeof(T)), "memset");
+    ck(cudaMallocHost((void**)&h_torque_, kMaxChunk * sizeof(unsigned long long)), "host alloc");
+    ck(cudaMallocHost((void**)&h_sums_, kMaxChunk * 8 * sizeof(double)), "host alloc");
+    ck(cudaMallocHost((void**)&h_err_, sizeof(int)), "host alloc");
+    ck(cudaMallocHost((void**)&h_stage_, 3 * n * sizeof(T)), "host alloc");
+
+    if (terms_.demag) {
+        const long long nrows = (long long)g.ny * g.nz;
+        alloc(&A_, 3 * nrows * geo_.Hp * sizeof(C2<T>));
+        alloc(&B_, 3 * (long long)g.nz * Py_ * geo_.Hp * sizeof(C2<T>));
+        alloc(&Kt_, 6 * (long long)Hy_ * Hz_ * geo_.Hp * sizeof(T));
+        alloc(&ybuf_, Hy_ * sizeof(int));
+        // twiddles exp(-2 pi i k / TWN), long double on the host, cast to T (fft.hpp:70-74)
+        std::vector<C2<T>> tw(TWN);
+        for (int k = 0; k < TWN; ++k) {
+            const long double a = -2.0L * (long double)kPi * k / TWN;
+            tw[k].x = static_cast<T>(cosl(a));
+            tw[k].y = static_cast<T>(sinl(a));
+        }
+        alloc(&tw_, TWN * sizeof(C2<T>));
+        ck(cudaMemcpy(tw_, tw.data(), TWN * sizeof(C2<T>), cudaMemcpyHostToDevice), "tw upload");
+        k_ybuf<T><<<(Hy_ + 127) / 128, 128, 0, stream_>>>(Py_, Hy_, ybuf_);
+        ck(cudaGetLastError(), "k_ybuf");
+        // shared-memory opt-in for the instantiations this grid uses
+        with_pow2(geo_.N, [&]<int L>() {
+            set_smem<T>((const void*)k_r2c_x<T, L>, XCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM);
+            k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
+        });
+        with_pow2(Py_, [&]<int L>() {
+            set_smem<T>((const void*)k_fft_y_fwd<T, L>, YCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_fft_y_inv<T, L>, YCfg<T, L>::SMEM);
+        });
+        with_pow2(Pz_, [&]<int L>() { set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM); });
+        // tensor octant on the device (K0a), then spectra (K0b)
+        alloc(&oct_, 6 * n * sizeof(double));
+        launch_tensor_octant(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, oct_, stream_);
+        ck(cudaGetLastError(), "k_tensor_octant");
+        build_tensor_from_octant();
+    } else {
+        k5_blocks_ = (n + 255) / 256;
+    }
+    alloc(&partials_, (size_t)k5_blocks_ * 8 * sizeof(double));
+    ck(cudaStreamSynchronize(stream_), "setup");
+}
+
+template <class T>
+Engine<T>::~Engine() {
+    cudaSetDevice(device_);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, oct_, err_, torque_, sums_, partials_, ticket_};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h_torque_) cudaFreeHost(h_torque_);
+    if (h_sums_) cudaFreeHost(h_sums_);
+    if (h_err_) cudaFreeHost(h_err_);
+    if (h_stage_) cudaFreeHost(h_stage_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+// K0b: separable cosine/sine transforms of the fp64 octant -> real spectrum octant in T.
+template <class T>
+void Engine<T>::build_tensor_from_octant() {
+    const int nx = grid_.nx, ny = grid_.ny, nz = grid_.nz;
+    const int Hx = geo_.Hx, Hp = geo_.Hp;
+    const long long n = geo_.ncell;
+    double *Cx[2], *Cy[2], *Cz[2], *T1, *T2;
+    auto mat = [&](double** C, int H, int nn, int P) {
+        for (int odd = 0; odd < 2; ++odd) {
+            ck(cudaMalloc((void**)&C[odd], (size_t)H * nn * sizeof(double)), "cudaMalloc");
+            launch_axis_matrix(H, nn, P, odd, C[odd], stream_);
+        }
+    };
+    mat(Cx, Hx, nx, geo_.Px);
+    mat(Cy, Hy_, ny, Py_);
+    mat(Cz, Hz_, nz, Pz_);
+    ck(cudaMalloc((void**)&T1, (size_t)nz * ny * Hx * sizeof(double)), "cudaMalloc");
+    ck(cudaMalloc((void**)&T2, (size_t)nz * Hy_ * Hx * sizeof(double)), "cudaMalloc");
+    // parity per component (xx,yy,zz,xy,xz,yz): odd along x / y / z
+    const int ox[6] = {0, 0, 0, 1, 1, 0}, oy[6] = {0, 0, 0, 1, 0, 1}, oz[6] = {0, 0, 0, 0, 1, 1};
+    for (int c = 0; c < 6; ++c) {
+        GemmDesc d{};
+        // x: T1[row][u] = sum_i E[row][i] Cx[u][i]
+        d = GemmDesc{};
+        d.Mdim = ny * nz; d.Ndim = Hx; d.Kdim = nx;
+        d.a_m = nx; d.a_k = 1; d.b_k = 1; d.b_n = nx; d.o_m = Hx; d.o_n = 1; d.nb2 = 1; d.scale = 1.0;
+        launch_gemm64(d, 1, oct_ + c * n, Cx[ox[c]], T1, stream_);
+        // y: T2[k][v][u] = sum_j Cy[v][j] T1[k][j][u]
+        d = GemmDesc{};
+        d.Mdim = Hy_; d.Ndim = Hx; d.Kdim = ny;
+        d.a_m = ny; d.a_k = 1; d.b_k = Hx; d.b_n = 1; d.o_m = Hx; d.o_n = 1;
+        d.b_b1 = (long long)ny * Hx; d.o_b1 = (long long)Hy_ * Hx; d.nb2 = 1; d.scale = 1.0;
+        launch_gemm64(d, nz, Cy[oy[c]], T1, T2, stream_);
+        // z: Kt[c][v][w][u] = s * sum_k Cz[w][k] T2[k][v][u];  two odd axes give (-2i)^2 = -4 -> s = -1
+        d = GemmDesc{};
+        d.Mdim = Hz_; d.Ndim = Hx; d.Kdim = nz;
+        d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = Hp; d.o_n = 1;
+        d.b_b1 = Hx; d.o_b1 = (long long)Hz_ * Hp; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
+        launch_gemm64(d, Hy_, Cz[oz[c]], T2, Kt_ + (long long)c * Hy_ * Hz_ * Hp, stream_);
+        ck(cudaGetLastError(), "tensor gemm");
+    }
+    ck(cudaStreamSynchronize(stream_), "tensor setup");
+    for (int odd = 0; odd < 2; ++odd) {
+        cudaFree(Cx[odd]);
+        cudaFree(Cy[odd]);
+        cudaFree(Cz[odd]);
+    }
+    cudaFree(T1);
+    cudaFree(T2);
+}
+
+template <class T>
+void Engine<T>::set_octant(const double* oct) {
+    if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    ck(cudaMemcpy(oct_, oct, 6 * geo_.ncell * sizeof(double), cudaMemcpyHostToDevice), "octant upload");
+    build_tensor_from_octant();
+}
+
+template <class T>
+void Engine<T>::get_octant(double* oct) {
+    if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    ck(cudaMemcpy(oct, oct_, 6 * geo_.ncell * sizeof(double), cudaMemcpyDeviceToHost), "octant download");
+}
+
+template <class T>
+void Engine<T>::get_spectrum(double* out) {
+    if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    const long long cnt = 6LL * Hy_ * Hz_ * geo_.Hp;
+    std::vector<T> h(cnt);
+    ck(cudaMemcpy(h.data(), Kt_, cnt * sizeof(T), cudaMemcpyDeviceToHost), "spectrum download");
+    const int Hx = geo_.Hx;
+    for (int c = 0; c < 6; ++c)
+        for (int v = 0; v < Hy_; ++v)
+            for (int w = 0; w < Hz_; ++w)
+                for (int u = 0; u < Hx; ++u)
+                    out[(((long long)c * Hy_ + v) * Hz_ + w) * Hx + u] =
+                        (double)h[(((long long)c * Hy_ + v) * Hz_ + w) * geo_.Hp + u];
+}
+
+// --------------------------------------------------------------- enqueue
+template <class T>
+void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
+    const T* Mc = M_[cur];
+    T* Mn = M_[cur ^ 1];
+    Ctl ctl{err_, it.check_prev && it.slot > 0 ? torque_ + it.slot - 1 : nullptr, mat_.Ms,
+            st_.torque_tol_deg_per_ns, kRadToDegPerNs};
+    StepIO io{};
+    io.update = it.update;
+    io.renorm = it.renorm;
+    io.write_h = it.write_h;
+    io.sums = it.sums;
+    io.iter = it.slot;
+    io.torque = torque_ + it.slot;
+    io.partials = partials_;
+    io.sums_out = sums_ + 8 * it.slot;
+    io.ticket = ticket_;
+    if (events) ck(cudaEventRecord(ev[0], stream_), "event");
+    if (!terms_.demag) {
+        k_local_llg<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(geo_, Mc, Mn, H_, lp_, io, ctl);
+        if (events)
+            for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
+        return;
+    }
+    const long long nrows = (long long)geo_.ny * geo_.nz;
+    with_pow2(geo_.N, [&]<int L>() {
+        using CF = XCfg<T, L>;
+        dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
+        k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Mc, A_, tw_, ctl);
+    });
+    if (events) ck(cudaEventRecord(ev[1], stream_), "event");
+    with_pow2(Py_, [&]<int L>() {
+        using CF = YCfg<T, L>;
+        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
+        k_fft_y_fwd<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
+    });
+    if (events) ck(cudaEventRecord(ev[2], stream_), "event");
+    with_pow2(Pz_, [&]<int L>() {
+        using CF = ZCfg<T, L>;
+        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
+        k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+    });
+    if (events) ck(cudaEventRecord(ev[3], stream_), "event");
+    with_pow2(Py_, [&]<int L>() {
+        using CF = YCfg<T, L>;
+        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
+        k_fft_y_inv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
+    });
+    if (events) ck(cudaEventRecord(ev[4], stream_), "event");
+    with_pow2(geo_.N, [&]<int L>() {
+        using CF = LCfg<T, L>;
+        dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
+        k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+    });
+    if (events) ck(cudaEventRecord(ev[5], stream_), "event");
+}
+
+// Launch a chunk of iterations (one CUDA graph, cached by its shape).
+template <class T>
+void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
+    auto key = std::make_pair(its, cur);
+    auto f = graphs_.find(key);
+    if (f == graphs_.end()) {
+        if (graphs_.size() > 64) {
+            for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+            graphs_.clear();
+        }
+        cudaGraph_t g;
+        ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+        cudaMemsetAsync(torque_, 0, its.size() * sizeof(unsigned long long), stream_);
+        int c = cur;
+        for (const Iter& it : its) {
+            enqueue(it, c);
+            if (it.update) c ^= 1;
+        }
+        ck(cudaStreamEndCapture(stream_, &g), "end capture");
+        cudaGraphExec_t ex;
+        ck(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        f = graphs_.emplace(key, ex).first;
+    }
+    ck(cudaGraphLaunch(f->second, stream_), "graph launch");
+}
+
+template <class T>
+void Engine<T>::fetch_chunk(int n, std::vector<double>& torque, int& err) {
+    ck(cudaMemcpyAsync(h_torque_, torque_, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaMemcpyAsync(h_sums_, sums_, (size_t)n * 8 * sizeof(double), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaMemcpyAsync(h_err_, err_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    torque.resize(n);
+    for (int i = 0; i < n; ++i) torque[i] = torque_of(h_torque_[i]);
+    err = *h_err_;
+    if (err) ck(cudaMemsetAsync(err_, 0, sizeof(int), stream_), "memset");
+}
+
+template <class T>
+double Engine<T>::torque_of(unsigned long long bits) const {
+    double r;
+    std::memcpy(&r, &bits, sizeof r);
+    return std::sqrt(r) / mat_.Ms * kRadToDegPerNs;   // dynamics.hpp:81
+}
+
+// --------------------------------------------------------------- state io
+template <class T>
+void Engine<T>::set_m(const double* x, const double* y, const double* z) {
+    const long long n = geo_.ncell;
+    for (long long i = 0; i < n; ++i) {
+        h_stage_[i] = static_cast<T>(x[i]);
+        h_stage_[i + n] = static_cast<T>(y[i]);
+        h_stage_[i + 2 * n] = static_cast<T>(z[i]);
+    }
+    ck(cudaMemcpyAsync(M_[cur_], h_stage_, 3 * n * sizeof(T), cudaMemcpyHostToDevice, stream_), "h2d");
+    ck(cudaStreamSynchronize(stream_), "sync");
+}
+template <class T>
+void Engine<T>::set_m32(const float* x, const float* y, const float* z) {
+    const long long n = geo_.ncell;
+    for (long long i = 0; i < n; ++i) {
+        h_stage_[i] = static_cast<T>(x[i]);
+        h_stage_[i + n] = static_cast<T>(y[i]);
+        h_stage_[i + 2 * n] = static_cast<T>(z[i]);
+    }
+    ck(cudaMemcpyAsync(M_[cur_], h_stage_, 3 * n * sizeof(T), cudaMemcpyHostToDevice, stream_), "h2d");
+    ck(cudaStreamSynchronize(stream_), "sync");
+}
+template <class T>
+void Engine<T>::get_m(double* x, double* y, double* z) {
+    const long long n = geo_.ncell;
+    ck(cudaMemcpyAsync(h_stage_, M_[cur_], 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    for (long long i = 0; i < n; ++i) {
+        x[i] = h_stage_[i];
+        y[i] = h_stage_[i + n];
+        z[i] = h_stage_[i + 2 * n];
+    }
+}
+template <class T>
+void Engine<T>::get_m32(float* x, float* y, float* z) {
+    const long long n = geo_.ncell;
+    ck(cudaMemcpyAsync(h_stage_, M_[cur_], 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    for (long long i = 0; i < n; ++i) {
+        x[i] = (float)h_stage_[i];
+        y[i] = (float)h_stage_[i + n];
+        z[i] = (float)h_stage_[i + 2 * n];
+    }
+}
+template <class T>
+void Engine<T>::set_uniform(const double dir[3]) {
+    // makeUniformState: (Ms * direction).cast<T>() (state.hpp:71-78)
+    const double Ms = mat_.Ms;
+    k_fill3<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
+        M_[cur_], geo_.ncell, static_cast<T>(Ms * dir[0]), static_cast<T>(Ms * dir[1]), static_cast<T>(Ms * dir[2]));
+    ck(cudaGetLastError(), "fill");
+    ck(cudaStreamSynchronize(stream_), "sync");
+}
+
+// One evaluation without update (H, torque and optionally the sample sums).
+template <class T>
+void Engine<T>::eval(int write_h, bool sums, double& torque, double sum_out[8]) {
+    Iter it;
+    it.update = 0;
+    it.renorm = 0;
+    it.write_h = write_h;
+    it.sums = sums;
+    it.slot = 0;
+    run_chunk({it}, cur_);
+    std::vector<double> tq;
+    int err = 0;
+    fetch_chunk(1, tq, err);
+    torque = tq[0];
+    if (sum_out) std::memcpy(sum_out, h_sums_, 8 * sizeof(double));
+}
+
+template <class T>
+void Engine<T>::field(int which, double* x, double* y, double* z) {
+    if (which == 2 && !terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    double tq;
+    eval(which, false, tq, nullptr);
+    const long long n = geo_.ncell;
+    ck(cudaMemcpyAsync(h_stage_, H_, 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    for (long long i = 0; i < n; ++i) {
+        x[i] = h_stage_[i];
+        y[i] = h_stage_[i + n];
+        z[i] = h_stage_[i + 2 * n];
+    }
+}
+
+// --------------------------------------------------------------- stepping
+// Simulation<T>::step x n: renormalise iff (step+1) % renormalizeEvery == 0 (sim.hpp:38).
+template <class T>
+void Engine<T>::step(long n, double* last, double* all) {
+    long done = 0;
+    std::vector<double> tq;
+    while (done < n) {
+        const int K = (int)std::min<long>(n - done, 64);
+        std::vector<Iter> its(K);
+        for (int i = 0; i < K; ++i) {
+            its[i].slot = i;
+            its[i].renorm = ((stepno + i + 1) % st_.renorm_every) == 0;
+        }
+        run_chunk(its, cur_);
+        int err = 0;
+        fetch_chunk(K, tq, err);
+        const int ok = err ? err - 1 : K;      // iterations that completed their update
+        for (int i = 0; i < ok; ++i) {
+            t += st_.dt;                        // dynamics.hpp:118-119
+            stepno += 1;
+            cur_ ^= 1;
+            if (all) all[done + i] = tq[i];
+        }
+        if (err) {
+            if (last) *last = tq[ok];
+            throw Error(MFD_ENONFINITE, "eulerUpdate: non-finite magnetization after step (time step too large?)");
+        }
+        done += K;
+        if (last) *last = tq[K - 1];
+    }
+}
+
+template <class T>
+void Engine<T>::step_async(long n) {
+    // Benchmark path: whole graphs of 64 steps, no host round trip; the
+    // renormalisation pattern is fixed per graph.
+    long done = 0;
+    while (done < n) {
+        const int K = (int)std::min<long>(n - done, 64);
+        std::vector<Iter> its(K);
+        for (int i = 0; i < K; ++i) {
+            its[i].slot = i;
+            its[i].renorm = ((stepno + i + 1) % st_.renorm_every) == 0;
+        }
+        run_chunk(its, cur_);
+        for (int i = 0; i < K; ++i) {
+            t += st_.dt;
+            stepno += 1;
+            cur_ ^= 1;
+        }
+        done += K;
+    }
+}
+
+template <class T>
+void Engine<T>::sync() {
+    ck(cudaMemcpyAsync(h_err_, err_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    if (*h_err_) {
+        cudaMemsetAsync(err_, 0, sizeof(int), stream_);
+        throw Error(MFD_ENONFINITE, "eulerUpdate: non-finite magnetization after step (time step too large?)");
+    }
+}
+
+template <class T>
+mfd_sample Engine<T>::make_sample(const double s[8], double torque) const {
+    // reducedMean (state.hpp:113-124) + energies (fields.hpp:127-190) from the device sums
+    mfd_sample o{};
+    o.step = stepno;
+    o.t = t;
+    const double sc = 1.0 / (mat_.Ms * (double)geo_.ncell);
+    o.m[0] = s[0] * sc;
+    o.m[1] = s[1] * sc;
+    o.m[2] = s[2] * sc;
+    const double V = lp_.dV;
+    o.e_exchange = (terms_.exchange && mat_.A > 0) ? s[3] * (mat_.A * V / (mat_.Ms * mat_.Ms)) : 0.0;
+    o.e_anisotropy = (terms_.anisotropy && mat_.Ku != 0) ? s[4] * (mat_.Ku * V) : 0.0;
+    o.e_demag = terms_.demag ? s[5] * (-0.5 * kMu0 * V) : 0.0;
+    const bool zee = terms_.zeeman && (terms_.h_ext[0] != 0 || terms_.h_ext[1] != 0 || terms_.h_ext[2] != 0);
+    o.e_zeeman = zee ? s[6] * (-kMu0 * V) : 0.0;
+    o.e_total = o.e_exchange + o.e_anisotropy + o.e_demag + o.e_zeeman;
+    o.torque_deg_per_ns = torque;
+    return o;
+}
+
+template <class T>
+mfd_sample Engine<T>::sample_now() {
+    double s[8], tq;
+    eval(0, true, tq, s);
+    return make_sample(s, tq);
+}
+
+// dynamics::relax (dynamics.hpp:157-198) in graph chunks.  Iteration i of a
+// chunk skips itself on the device once iteration i-1 met the torque
+// criterion, so the stop step is exactly the reference's; sample iterations
+// (iter % sampleEvery == 0) reduce <m> and the energies inside K5.
+template <class T>
+bool Engine<T>::relax(mfd_sample_cb cb, void* user) {
+    if (!(st_.dt > 0)) throw Error(MFD_EINVAL, "StepperConfig: dt must be > 0");
+    const long startStep = stepno;
+    long iter = 0;
+    const long sampleEvery = st_.sample_every > 0 ? st_.sample_every : 1;
+    std::vector<double> tq;
+    while (true) {
+        if (iter >= st_.max_steps) {
+            // exhausted: evaluate, sample, stop (converged if the torque is within tolerance)
+            double s[8], torque;
+            eval(0, true, torque, s);
+            mfd_sample smp = make_sample(s, torque);
+            if (cb) cb(&smp, user);
+            return torque <= st_.torque_tol_deg_per_ns;
+        }
+        const int K = (int)std::min<long>(st_.max_steps - iter, std::min<long>(kMaxChunk, 128));
+        std::vector<Iter> its(K);
+        for (int i = 0; i < K; ++i) {
+            its[i].slot = i;
+            its[i].check_prev = 1;
+            its[i].sums = ((iter + i) % sampleEvery) == 0;
+            its[i].renorm = ((stepno + i + 1 - startStep) % st_.renorm_every) == 0;   // dynamics.hpp:192
+        }
+        run_chunk(its, cur_);
+        int err = 0;
+        fetch_chunk(K, tq, err);
+        for (int i = 0; i < K; ++i) {
+            const bool converged = tq[i] <= st_.torque_tol_deg_per_ns;
+            if (converged) {
+                double s[8], torque;
+                eval(0, true, torque, s);        // same state, same H: the iteration's sample
+                mfd_sample smp = make_sample(s, torque);
+                if (cb) cb(&smp, user);
+                return true;
+            }
+            if (its[i].sums && cb) {
+                mfd_sample smp = make_sample(h_sums_ + 8 * i, tq[i]);
+                cb(&smp, user);
+            }
+            if (err && i == err - 1)
+                throw Error(MFD_ENONFINITE, "eulerUpdate: non-finite magnetization after step (time step too large?)");
+            t += st_.dt;
+            stepno += 1;
+            cur_ ^= 1;
+        }
+        iter += K;
+    }
+}
+
+template <class T>
+void Engine<T>::timing(double ms[7]) {
+    cudaEvent_t ev[6];
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    Iter it;
+    it.update = 0;
+    it.renorm = 0;
+    enqueue(it, cur_, true, ev);
+    ck(cudaStreamSynchronize(stream_), "sync");
+    for (int q = 0; q < 5; ++q) {
+        float f = 0;
+        cudaEventElapsedTime(&f, ev[q], ev[q + 1]);
+        ms[q] = f;
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev[0], ev[5]);
+    ms[5] = tot;
+    ms[6] = 0;
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
+// Algorithmic HBM bytes per step, 5-pass model.
+template <class T>
+double Engine<T>::model_bytes() const {
+    const double s = sizeof(T), c = 2 * s, N = (double)geo_.ncell;
+    if (!terms_.demag) return 3 * N * s * 2 + 6 * N * s;   // read M (7-pt, cached) + write M
+    const double Hx = geo_.Hx, ny = geo_.ny, nz = geo_.nz;
+    const double k1 = 3 * N * s + 3 * Hx * ny * nz * c;
+    const double k2 = 3 * Hx * ny * nz * c + 3 * Hx * Py_ * nz * c;
+    const double k3 = 2 * (3 * Hx * Py_ * nz * c) + 6 * Hx * Hy_ * Hz_ * s;
+    const double k4 = k2;
+    const double k5 = 3 * Hx * ny * nz * c + 3 * N * s + 3 * N * s;
+    return k1 + k2 + k3 + k4 + k5;
+}
+
+} // namespace mfd

@@ -1,0 +1,190 @@
+// Mixed-radix Stockham FFT engine for batches of power-of-two columns held by
+// one CTA.  Replaces the reference's iterative radix-2 LineTransform
+// (proj/include/magfd/fft.hpp:54-121): same unnormalised DFT convention
+// (forward exp(-2 pi i nk/L), inverse conjugate twiddles), but organised as
+// 1-3 register-radix stages with the data moved through shared memory (or
+// straight from / to HBM on the first / last stage), so a length-1024 column
+// costs one global read, one shared-memory round trip and one global write.
+//
+// Stage s (radix R, sub-length M, Mp = M/R) of the forward (DIT) transform,
+// for task (p, n2):   out[p*M + Mp*k + n2] = W_M^{n2 k} * sum_n1 in[p*M + Mp*n1 + n2] W_R^{n1 k}
+// After all stages, frequency f = k0 + R0*(k1 + R1*k2) sits at buffer
+// position bufpos(f) = k0*Mp0 + k1*Mp1 + k2*Mp2 (mixed-radix digit reversal).
+// The inverse runs the transposed stages in reverse order: it consumes
+// buffer order and produces natural order, so no explicit reordering pass
+// is ever needed.
+#pragma once
+#include "common.cuh"
+
+namespace mfd {
+
+// Radix plans: at most 32 complex values per task in fp32, 16 in fp64.
+template <class T, int L> struct Plan;
+#define MFD_PLAN(TT, L_, S_, A_, B_, C_)                                    \
+    template <> struct Plan<TT, L_> {                                      \
+        static constexpr int S = S_, R0 = A_, R1 = B_, R2 = C_;            \
+    };
+MFD_PLAN(float, 1, 0, 1, 1, 1)
+MFD_PLAN(float, 2, 1, 2, 1, 1)
+MFD_PLAN(float, 4, 1, 4, 1, 1)
+MFD_PLAN(float, 8, 1, 8, 1, 1)
+MFD_PLAN(float, 16, 1, 16, 1, 1)
+MFD_PLAN(float, 32, 1, 32, 1, 1)
+MFD_PLAN(float, 64, 2, 8, 8, 1)
+MFD_PLAN(float, 128, 2, 16, 8, 1)
+MFD_PLAN(float, 256, 2, 16, 16, 1)
+MFD_PLAN(float, 512, 2, 32, 16, 1)
+MFD_PLAN(float, 1024, 2, 32, 32, 1)
+MFD_PLAN(float, 2048, 3, 16, 16, 8)
+MFD_PLAN(double, 1, 0, 1, 1, 1)
+MFD_PLAN(double, 2, 1, 2, 1, 1)
+MFD_PLAN(double, 4, 1, 4, 1, 1)
+MFD_PLAN(double, 8, 1, 8, 1, 1)
+MFD_PLAN(double, 16, 1, 16, 1, 1)
+MFD_PLAN(double, 32, 2, 8, 4, 1)
+MFD_PLAN(double, 64, 2, 8, 8, 1)
+MFD_PLAN(double, 128, 2, 16, 8, 1)
+MFD_PLAN(double, 256, 2, 16, 16, 1)
+MFD_PLAN(double, 512, 3, 16, 8, 4)
+MFD_PLAN(double, 1024, 3, 16, 8, 8)
+MFD_PLAN(double, 2048, 3, 16, 16, 8)
+#undef MFD_PLAN
+
+template <class T, int L, int s> struct StageInfo {
+    using P = Plan<T, L>;
+    static constexpr int R = s == 0 ? P::R0 : s == 1 ? P::R1 : P::R2;
+    static constexpr int PRE = s == 0 ? 1 : s == 1 ? P::R0 : P::R0 * P::R1;
+    static constexpr int M = L / PRE;
+    static constexpr int MP = M / R;
+};
+
+// Buffer position of natural frequency f after the forward stages.
+template <class T, int L>
+__device__ __forceinline__ int bufpos(int f) {
+    using P = Plan<T, L>;
+    if constexpr (P::S == 0) {
+        return 0;
+    } else if constexpr (P::S == 1) {
+        return f;
+    } else if constexpr (P::S == 2) {
+        const int k0 = f % P::R0, k1 = f / P::R0;
+        return k0 * StageInfo<T, L, 0>::MP + k1;
+    } else {
+        const int k0 = f % P::R0, r = f / P::R0;
+        const int k1 = r % P::R1, k2 = r / P::R1;
+        return k0 * StageInfo<T, L, 0>::MP + k1 * StageInfo<T, L, 1>::MP + k2;
+    }
+}
+
+// Twiddle W_M^{e} (forward sign) from the global table of TWN entries.
+constexpr int TWN = 4096;
+template <class T, int M>
+__device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) {
+    return __ldg(tw + e * (TWN / M));
+}
+
+// One stage over NCOL columns with NT threads.
+//   INV=false: forward DIT stage (gather in-positions, DFT, twiddle, scatter out-positions)
+//   INV=true : transposed inverse stage (gather out-positions, conj twiddle, IDFT, scatter in-positions)
+// COLFAST: consecutive threads take consecutive columns (y/z passes: columns
+// are contiguous in HBM); otherwise consecutive threads take consecutive
+// tasks of one column (x pass: positions contiguous in HBM).
+// SYNC_MID inserts a barrier between the gather and scatter phases, required
+// when source and destination are the same shared buffer.
+template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, class LD,
+          class ST>
+__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw) {
+    using SI = StageInfo<T, L, s>;
+    constexpr int R = SI::R, M = SI::M, MP = SI::MP;
+    constexpr int TPC = L / R;
+    constexpr int TOTAL = NCOL * TPC;
+    constexpr int TPT = (TOTAL + NT - 1) / NT;
+    C2<T> v[TPT][R];
+    int colv[TPT], basev[TPT], n2v[TPT];
+#pragma unroll
+    for (int i = 0; i < TPT; ++i) {
+        const int q = threadIdx.x + i * NT;
+        int col, t;
+        if (COLFAST) { col = q % NCOL; t = q / NCOL; }
+        else { t = q % TPC; col = q / TPC; }
+        const int p = t / MP, n2 = t % MP;
+        colv[i] = col;
+        basev[i] = p * M + n2;
+        n2v[i] = n2;
+        if (TOTAL % NT == 0 || q < TOTAL) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[i][j] = ld(col, basev[i] + MP * j);
+        }
+    }
+    if (SYNC_MID) __syncthreads();
+#pragma unroll
+    for (int i = 0; i < TPT; ++i) {
+        const int q = threadIdx.x + i * NT;
+        if (TOTAL % NT == 0 || q < TOTAL) {
+            if (!INV) {
+                dft<T, R, false>(v[i]);
+                if (MP > 1) {
+#pragma unroll
+                    for (int k = 1; k < R; ++k) v[i][k] = cmul<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
+                }
+            } else {
+                if (MP > 1) {
+#pragma unroll
+                    for (int k = 1; k < R; ++k) v[i][k] = cmulc<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
+                }
+                dft<T, R, true>(v[i]);
+            }
+#pragma unroll
+            for (int j = 0; j < R; ++j) st(colv[i], basev[i] + MP * j, v[i][j]);
+        }
+    }
+}
+
+// Full forward transform: stage 0 reads via ld0, the last stage writes via
+// stN, intermediate stages go through shared memory via (lds, sts).
+// FIRST_SMEM / LAST_SMEM say whether ld0 / stN touch that same shared buffer,
+// in which case the stage gathers everything before a barrier and scatters
+// after it (in-place Stockham).  A barrier follows every shared-memory write.
+template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, class LD0,
+          class LDS, class STS, class STN>
+__device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
+                                            const C2<T>* __restrict__ tw) {
+    constexpr int S = Plan<T, L>::S;
+    if constexpr (S == 1) {
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM>(ld0, stn, tw);
+    } else if constexpr (S == 2) {
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+    } else if constexpr (S == 3) {
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, true>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 2, false, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+    }
+}
+
+// Full inverse (transposed) transform: consumes buffer order via ld0,
+// produces natural order via stN.
+template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, class LD0,
+          class LDS, class STS, class STN>
+__device__ __forceinline__ void fft_inverse(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
+                                            const C2<T>* __restrict__ tw) {
+    constexpr int S = Plan<T, L>::S;
+    if constexpr (S == 1) {
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM>(ld0, stn, tw);
+    } else if constexpr (S == 2) {
+        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+    } else if constexpr (S == 3) {
+        fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, true>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+    }
+}
+
+} // namespace mfd

@@ -1,0 +1,532 @@
+// Per-step kernels of the demag convolution + fused LLG update.
+//
+//   K1 k_r2c_x        M rows -> half spectrum along x        (pad fused; demag.hpp:204-228, fft.hpp:201-210)
+//   K2 k_fft_y_fwd    y transform of the ny active rows       (fft.hpp:213-220)
+//   K3 k_fft_z_conv   z transform -> K~ . M~ -> inverse z     (fft.hpp:223-237, demag.hpp:150-171)
+//   K4 k_fft_y_inv    inverse y, keep ny rows                 (fft.hpp:181-186)
+//   K5 k_c2r_x_llg    inverse x -> H_demag -> H_eff -> LLG -> Euler -> reductions
+//                     (demag.hpp:237-249, fields.hpp:220-253, dynamics.hpp:49-121)
+//
+// HBM layout (T = float or double, C2<T> = complex):
+//   M      3 x N  SoA, x fastest (grid.hpp:30-34), double-buffered
+//   A      [3][nz][ny][Hp]  complex   x-spectrum of the active rows (Hp >= Px/2+1)
+//   B      [3][nz][Py][Hp]  complex   x,y-spectrum, y in buffer (digit-reversed) order
+//   Kt     [6][Py/2+1][Pz/2+1][Hp] T  real tensor spectrum octant (xx,yy,zz,xy,xz,yz)
+#pragma once
+#include "fft_engine.cuh"
+
+namespace mfd {
+
+template <class T> constexpr int regE() { return sizeof(T) == 4 ? 32 : 16; }
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int clampNT(int n) { return n < 32 ? 32 : n > 1024 ? 1024 : n; }
+// x-pass shared layout [col][pos] with one pad element every 128 B.
+template <class T> constexpr int padShift() { return sizeof(T) == 4 ? 4 : 3; }
+template <class T> __device__ __forceinline__ int xpad(int pos) { return pos + (pos >> padShift<T>()); }
+template <class T, int L> constexpr int xpitch() { return L + (L >> padShift<T>()) + 1; }
+
+// -------------------------------------------------------------- configs
+template <class T, int N> struct XCfg {   // K1
+    static constexpr int E = regE<T>();
+    static constexpr int ROWS = cmax(1, cmin(64, 256 * E / N));
+    static constexpr int NT = clampNT(cmax(128, ROWS * N / E));
+    static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
+};
+template <class T, int N> struct LCfg {   // K5
+    static constexpr int ROWS = cmax(1, cmin(32, 2048 / cmax(N, 1)));
+    static constexpr int NT = 256;
+    static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
+};
+template <class T, int L> struct YCfg {   // K2 / K4
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr int W = cmax(1, cmin(128 / CS, 131072 / (L * CS)));
+    static constexpr int NT = clampNT(W * L / regE<T>());
+    static constexpr int SMEM = Plan<T, L>::S >= 2 ? W * L * CS : 0;
+};
+template <class T, int L> struct ZCfg {   // K3
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr int W = cmax(1, cmin(128 / CS, 98304 / (6 * L * CS)));
+    static constexpr int NCOL = 6 * W;
+    static constexpr int NT = clampNT(NCOL * L / regE<T>());
+    static constexpr int SMEM = NCOL * L * CS;
+};
+
+struct Geo {
+    int nx, ny, nz;
+    int Px, Py, Pz;
+    int N;     // Px/2 complex points per x row
+    int Hx;    // N + 1 bins
+    int Hp;    // padded pitch of A/B/Kt rows
+    long long ncell;
+};
+
+// Step control: early exit after a non-finite update (error) or, in relax
+// mode, once the previous iteration met the torque criterion
+// (dynamics.hpp:180-188).
+struct Ctl {
+    int* err;                                   // 0 ok, else failing iteration + 1
+    const unsigned long long* prev_torque;      // null: no convergence check
+    double Ms, tol, rad2deg;
+};
+__device__ __forceinline__ bool halted(const Ctl& c) {
+    if (*(volatile int*)c.err) return true;
+    if (c.prev_torque) {
+        const double r = __longlong_as_double((long long)*(volatile unsigned long long*)c.prev_torque);
+        if (sqrt(r) / c.Ms * c.rad2deg <= c.tol) return true;
+    }
+    return false;
+}
+
+// ------------------------------------------------------------------ K1
+template <class T, int N>
+__global__ void __launch_bounds__(XCfg<T, N>::NT)
+k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+    using CF = XCfg<T, N>;
+    constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>();
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const int comp = blockIdx.y;
+    const long long nrows = (long long)g.ny * g.nz;
+    const long long row0 = (long long)blockIdx.x * ROWS;
+    const T* Mc = M + comp * g.ncell;
+    const int nx = g.nx;
+    const bool even = (nx & 1) == 0;
+
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        const long long row = row0 + col;
+        const int i0 = 2 * pos;
+        if (row >= nrows || i0 >= nx) return mk<T>(0, 0);
+        const T* src = Mc + row * nx + i0;
+        if (even) {
+            return *reinterpret_cast<const C2<T>*>(src);
+        }
+        return mk<T>(src[0], i0 + 1 < nx ? src[1] : T(0));
+    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
+    if constexpr (Plan<T, N>::S == 0) {
+        for (int c = threadIdx.x; c < ROWS; c += NT) sts(c, 0, ld0(c, 0));
+    } else {
+        fft_forward<T, N, ROWS, NT, false, false, true>(ld0, lds, sts, sts, tw);
+    }
+    __syncthreads();
+    // Real-to-complex post-process: X[k] = E + W^k O, X[N-k] = conj(E - W^k O).
+    constexpr int HALF = N / 2 + 1;
+    for (int e = threadIdx.x; e < ROWS * HALF; e += NT) {
+        const int col = e / HALF, k = e % HALF;
+        const long long row = row0 + col;
+        if (row >= nrows) continue;
+        const C2<T> zk = sm[col * LP + xpad<T>(bufpos<T, N>(k % N))];
+        const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>(bufpos<T, N>((N - k) % N))]);
+        const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
+        const C2<T> d = csub<T>(zk, zn);
+        const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
+        const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));        // W_Px^k
+        const C2<T> wo = cmul<T>(w, O);
+        C2<T>* dst = A + ((long long)comp * nrows + row) * g.Hp;
+        dst[k] = cadd<T>(E, wo);
+        if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
+    }
+}
+
+// ------------------------------------------------------------------ K2
+template <class T, int L>
+__global__ void __launch_bounds__(YCfg<T, L>::NT)
+k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl) {
+    using CF = YCfg<T, L>;
+    constexpr int W = CF::W, NT = CF::NT;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const int u0 = blockIdx.x * W;
+    const int k = blockIdx.y, comp = blockIdx.z;
+    const C2<T>* src = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
+    C2<T>* dst = B + ((long long)comp * g.nz + k) * L * g.Hp + u0;
+    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx;
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        if (pos >= ny || u0 + col >= Hx) return mk<T>(0, 0);
+        return src[(long long)pos * Hp + col];
+    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
+    auto stn = [&](int col, int pos, C2<T> v) {
+        if (u0 + col < Hx) dst[(long long)pos * Hp + col] = v;
+    };
+    fft_forward<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
+}
+
+// ------------------------------------------------------------------ K4
+template <class T, int L>
+__global__ void __launch_bounds__(YCfg<T, L>::NT)
+k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+    using CF = YCfg<T, L>;
+    constexpr int W = CF::W, NT = CF::NT;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const int u0 = blockIdx.x * W;
+    const int k = blockIdx.y, comp = blockIdx.z;
+    const C2<T>* src = B + ((long long)comp * g.nz + k) * L * g.Hp + u0;
+    C2<T>* dst = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
+    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx;
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        if (u0 + col >= Hx) return mk<T>(0, 0);
+        return src[(long long)pos * Hp + col];
+    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
+    auto stn = [&](int col, int pos, C2<T> v) {
+        if (pos < ny && u0 + col < Hx) dst[(long long)pos * Hp + col] = v;
+    };
+    fft_inverse<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
+}
+
+// ------------------------------------------------------------------ K3
+// One CTA: W x-bins, the y-frequency pair {v, Py-v}, all three components,
+// full z columns.  Forward z (nz active inputs) -> per-bin symmetric real
+// 3x3 product with the tensor octant (mirror signs applied on the fly) ->
+// inverse z (nz outputs kept).  Nothing padded in z touches HBM.
+template <class T, int L>
+__global__ void __launch_bounds__(ZCfg<T, L>::NT)
+k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
+             const int* __restrict__ ybuf, Ctl ctl) {
+    using CF = ZCfg<T, L>;
+    constexpr int W = CF::W, NCOL = CF::NCOL, NT = CF::NT;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const int u0 = blockIdx.x * W;
+    const int v = blockIdx.y;                    // 0..Py/2
+    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int vp = (Py - v) & (Py - 1);
+    const bool pair = vp != v;
+    const long long rowA = ybuf[v], rowB = ybuf[vp];   // buffer rows of v and Py-v
+    const long long cstride = (long long)nz * Py * Hp; // component stride in B
+    const long long kstride = (long long)Py * Hp;      // z-plane stride in B
+    // column c = comp*2W + r*W + w  (r: 0 -> v, 1 -> Py-v)
+    auto gaddr = [&](int col, int pos) -> long long {
+        const int comp = col / (2 * W), r = (col / W) & 1, w = col % W;
+        return comp * cstride + (long long)pos * kstride + (r ? rowB : rowA) * Hp + u0 + w;
+    };
+    auto valid = [&](int col) { return u0 + (col % W) < Hx && (pair || ((col / W) & 1) == 0); };
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        if (pos >= nz || !valid(col)) return mk<T>(0, 0);
+        return B[gaddr(col, pos)];
+    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * NCOL + col]; };
+    auto sts = [&](int col, int pos, C2<T> val) { sm[pos * NCOL + col] = val; };
+    auto stn = [&](int col, int pos, C2<T> val) {
+        if (pos < nz && valid(col)) B[gaddr(col, pos)] = val;
+    };
+    fft_forward<T, L, NCOL, NT, true, false, true>(ld0, lds, sts, sts, tw);
+    __syncthreads();
+    // K~ . M~ : thread task (w, wq) covers z-frequencies {wq, Pz-wq} and both y rows.
+    const int Hy = Py / 2 + 1, Hz = L / 2 + 1;
+    const long long kcomp = (long long)Hy * Hz * Hp;
+    const T* kbase = Kt + ((long long)v * Hz) * Hp + u0;
+    for (int e = threadIdx.x; e < W * Hz; e += NT) {
+        const int w = e % W, wq = e / W;
+        if (u0 + w >= Hx) continue;
+        const T* kp = kbase + (long long)wq * Hp + w;
+        const T kxx = __ldg(kp), kyy = __ldg(kp + kcomp), kzz = __ldg(kp + 2 * kcomp);
+        const T kxy = __ldg(kp + 3 * kcomp), kxz = __ldg(kp + 4 * kcomp), kyz = __ldg(kp + 5 * kcomp);
+        const int wpart = (L - wq) & (L - 1);
+        const int nzf = wpart != wq ? 2 : 1;
+        const int nr = pair ? 2 : 1;
+        for (int zi = 0; zi < nzf; ++zi) {
+            const int wf = zi ? wpart : wq;
+            const T sz = zi ? T(-1) : T(1);
+            const int pos = bufpos<T, L>(wf);
+            for (int r = 0; r < nr; ++r) {
+                const T sy = r ? T(-1) : T(1);
+                C2<T>* s = sm + pos * NCOL + r * W + w;
+                const C2<T> mx = s[0], my = s[2 * W], mz = s[4 * W];
+                const T cxy = sy * kxy, cxz = sz * kxz, cyz = sy * sz * kyz;
+                s[0] = mk<T>(kxx * mx.x + cxy * my.x + cxz * mz.x, kxx * mx.y + cxy * my.y + cxz * mz.y);
+                s[2 * W] = mk<T>(cxy * mx.x + kyy * my.x + cyz * mz.x, cxy * mx.y + kyy * my.y + cyz * mz.y);
+                s[4 * W] = mk<T>(cxz * mx.x + cyz * my.x + kzz * mz.x, cxz * mx.y + cyz * my.y + kzz * mz.y);
+            }
+        }
+    }
+    __syncthreads();
+    fft_inverse<T, L, NCOL, NT, true, true, false>(lds, lds, sts, stn, tw);
+}
+
+// ------------------------------------------------------------------ K5
+// Local fields + LLG + Euler on one cell, in the reference's operation order
+// without FMA contraction (fields.hpp:33-48, 72-76, 246-250; dynamics.hpp:58-62, 101-108).
+template <class T> struct LocalParams {
+    T cx, cy, cz;          // exchange 2A/(mu0 Ms^2)/d^2 (fields.hpp:25-27)
+    int exch, anis, zee;   // gates (fields.hpp:239-245)
+    T ca;                  // 2Ku/(mu0 Ms^2)
+    T ax, ay, az;          // easy axis
+    T hx, hy, hz;          // uniform external field
+    T precess, damp, mu0;  // LLG (dynamics.hpp:54-57)
+    T dt, Ms;
+    double dA, dMs, dKu, dV;   // energy scalars (double)
+    double dax, day, daz, dhx, dhy, dhz;
+    double wx, wy, wz;     // 1/d^2 (fields.hpp:147-148)
+};
+
+struct StepIO {
+    int update;            // write M_new
+    int renorm;            // renormalise this step
+    int write_h;           // 0 none, 1 H_eff, 2 H_demag
+    int sums;              // accumulate sample sums
+    int iter;              // iteration index stored in err on failure
+    unsigned long long* torque;   // max |rhs|^2 bits
+    double* partials;      // [gridDim.x][8]
+    double* sums_out;      // [8]
+    unsigned int* ticket;
+};
+
+template <class T>
+__device__ __forceinline__ void cell_update(const Geo& g, const LocalParams<T>& P, const StepIO& io,
+                                            const T* __restrict__ M, T* __restrict__ Mn,
+                                            T* __restrict__ Hout, long long c, int i, int j, int k,
+                                            T hdx, T hdy, T hdz, double& tmax, double* acc,
+                                            int& bad) {
+    const long long n = g.ncell;
+    const T mx = M[c], my = M[c + n], mz = M[c + 2 * n];
+    T Hx = hdx, Hy = hdy, Hz = hdz;
+    double elink = 0;
+    if (P.exch) {
+        T h0 = 0, h1 = 0, h2 = 0;
+        const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+        auto add = [&](long long nb, T w) {
+            h0 = add_rn(h0, mul_rn(w, sub_rn(M[nb], mx)));
+            h1 = add_rn(h1, mul_rn(w, sub_rn(M[nb + n], my)));
+            h2 = add_rn(h2, mul_rn(w, sub_rn(M[nb + 2 * n], mz)));
+        };
+        auto link = [&](long long nb, double w) {
+            const double e0 = (double)M[nb] - mx, e1 = (double)M[nb + n] - my, e2 = (double)M[nb + 2 * n] - mz;
+            elink += w * (e0 * e0 + e1 * e1 + e2 * e2);
+        };
+        if (i > 0) add(c - 1, P.cx);
+        if (i < g.nx - 1) { add(c + 1, P.cx); if (io.sums) link(c + 1, P.wx); }
+        if (j > 0) add(c - sy, P.cy);
+        if (j < g.ny - 1) { add(c + sy, P.cy); if (io.sums) link(c + sy, P.wy); }
+        if (k > 0) add(c - sz, P.cz);
+        if (k < g.nz - 1) { add(c + sz, P.cz); if (io.sums) link(c + sz, P.wz); }
+        Hx = add_rn(Hx, h0);
+        Hy = add_rn(Hy, h1);
+        Hz = add_rn(Hz, h2);
+    }
+    if (P.anis) {
+        const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
+        Hx = add_rn(Hx, mul_rn(proj, P.ax));
+        Hy = add_rn(Hy, mul_rn(proj, P.ay));
+        Hz = add_rn(Hz, mul_rn(proj, P.az));
+    }
+    if (P.zee) {
+        Hx = add_rn(Hx, P.hx);
+        Hy = add_rn(Hy, P.hy);
+        Hz = add_rn(Hz, P.hz);
+    }
+    if (io.write_h == 1) {
+        Hout[c] = Hx; Hout[c + n] = Hy; Hout[c + 2 * n] = Hz;
+    } else if (io.write_h == 2) {
+        Hout[c] = hdx; Hout[c + n] = hdy; Hout[c + 2 * n] = hdz;
+    }
+    if (io.sums) {
+        acc[0] += (double)mx;
+        acc[1] += (double)my;
+        acc[2] += (double)mz;
+        acc[3] += elink;
+        const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
+        const double p = m0 * P.dax + m1 * P.day + m2 * P.daz;
+        acc[4] += 1.0 - p * p;
+        acc[5] += (double)hdx * mx + (double)hdy * my + (double)hdz * mz;
+        acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
+    }
+    // llgRhs: h = mu0*H; mxh = m x h; rhs = precess*mxh + damp*(m x mxh)
+    const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
+    const T c0 = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
+    const T c1 = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
+    const T c2 = sub_rn(mul_rn(mx, b1), mul_rn(my, b0));
+    const T d0 = sub_rn(mul_rn(my, c2), mul_rn(mz, c1));
+    const T d1 = sub_rn(mul_rn(mz, c0), mul_rn(mx, c2));
+    const T d2 = sub_rn(mul_rn(mx, c1), mul_rn(my, c0));
+    const T r0 = add_rn(mul_rn(P.precess, c0), mul_rn(P.damp, d0));
+    const T r1 = add_rn(mul_rn(P.precess, c1), mul_rn(P.damp, d1));
+    const T r2 = add_rn(mul_rn(P.precess, c2), mul_rn(P.damp, d2));
+    {
+        const double v0 = r0, v1 = r1, v2 = r2;
+        const double t2 = __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2));
+        tmax = fmax(tmax, t2);
+    }
+    if (io.update) {
+        T e0 = add_rn(mx, mul_rn(P.dt, r0));
+        T e1 = add_rn(my, mul_rn(P.dt, r1));
+        T e2 = add_rn(mz, mul_rn(P.dt, r2));
+        if (io.renorm) {
+            const T n2 = add_rn(add_rn(mul_rn(e0, e0), mul_rn(e1, e1)), mul_rn(e2, e2));
+            if (!(n2 > T(0)) || !isfinite((double)n2)) { bad = 1; return; }
+            const T f = P.Ms / sqrt(n2);
+            e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
+        } else if (!isfinite((double)add_rn(add_rn(e0, e1), e2))) {
+            bad = 1;
+            return;
+        }
+        Mn[c] = e0; Mn[c + n] = e1; Mn[c + 2 * n] = e2;
+    }
+}
+
+// Block-level epilogue shared by K5 and the demag-free kernel: torque max
+// (exact; one atomicMax on the ordered bit pattern), error flag, and the
+// deterministic two-level sample sums (fixed tree per block, last block
+// combines the per-block partials in index order).
+template <int NT>
+__device__ __forceinline__ void block_finish(const StepIO& io, const Ctl& ctl, double tmax, double* acc,
+                                             int bad) {
+    __shared__ double red[NT / 32][8];
+    __shared__ int anybad;
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) anybad = 0;
+    __syncthreads();
+    if (bad) anybad = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    if (io.sums) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    }
+    if (lane == 0) {
+        red[wid][7] = tmax;
+        if (io.sums)
+            for (int q = 0; q < 7; ++q) red[wid][q] = acc[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0][7];
+        for (int w = 1; w < NT / 32; ++w) t = fmax(t, red[w][7]);
+        atomicMax(io.torque, (unsigned long long)__double_as_longlong(t));
+        if (anybad) atomicCAS(ctl.err, 0, io.iter + 1);
+        if (io.sums) {
+            double* p = io.partials + (long long)(blockIdx.x + (long long)gridDim.x * blockIdx.y) * 8;
+            for (int q = 0; q < 7; ++q) {
+                double s = red[0][q];
+                for (int w = 1; w < NT / 32; ++w) s += red[w][q];
+                p[q] = s;
+            }
+            __threadfence();
+            const unsigned int total = gridDim.x * gridDim.y;
+            last = atomicAdd(io.ticket, 1u) == total - 1;
+        }
+    }
+    if (!io.sums) return;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const unsigned int total = gridDim.x * gridDim.y;
+    // fixed-order final combine: thread t sums partials t, t+NT, ... in order; then tree
+    __shared__ double fin[NT][7];
+    for (int q = 0; q < 7; ++q) {
+        double s = 0;
+        for (unsigned int b = threadIdx.x; b < total; b += NT) s += ((volatile double*)io.partials)[b * 8 + q];
+        fin[threadIdx.x][q] = s;
+    }
+    __syncthreads();
+    for (int w = NT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 7; ++q) fin[threadIdx.x][q] += fin[threadIdx.x + w][q];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 7; ++q) io.sums_out[q] = fin[0][q];
+        *io.ticket = 0;
+    }
+}
+
+template <class T, int N>
+__global__ void __launch_bounds__(LCfg<T, N>::NT)
+k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
+            T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io,
+            Ctl ctl) {
+    using CF = LCfg<T, N>;
+    constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const long long nrows = (long long)g.ny * g.nz;
+    const long long row0 = (long long)blockIdx.x * ROWS;
+    // Complex-to-real pre-process (pairs k, N-k): Z[k] = (X[k] + conj X[N-k]) + i W^-k (X[k] - conj X[N-k]),
+    // written at buffer positions so the transposed inverse stages emit natural order.
+    constexpr int HALF = N / 2 + 1;
+    for (int e = threadIdx.x; e < NCOL * HALF; e += NT) {
+        const int col = e / HALF, k = e % HALF;
+        const int comp = col / ROWS, r = col % ROWS;
+        const long long row = row0 + r;
+        C2<T> a = mk<T>(0, 0), b = mk<T>(0, 0);
+        if (row < nrows) {
+            const C2<T>* src = A + ((long long)comp * nrows + row) * g.Hp;
+            a = src[k];
+            b = src[N - k];
+        }
+        const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));   // W_Px^k, used conjugated
+        {
+            const C2<T> s = cadd<T>(a, cconj<T>(b)), d = csub<T>(a, cconj<T>(b));
+            const C2<T> wd = cmulc<T>(d, w);                     // W^-k d
+            sm[col * LP + xpad<T>(bufpos<T, N>(k % N))] = mk<T>(s.x - wd.y, s.y + wd.x);
+        }
+        if (N - k != k && N - k < N) {
+            const C2<T> s = cadd<T>(b, cconj<T>(a)), d = csub<T>(b, cconj<T>(a));
+            const C2<T> wn = mk<T>(-w.x, w.y);                  // W_Px^{N-k} = -conj(W^k)
+            const C2<T> wd = cmulc<T>(d, wn);
+            sm[col * LP + xpad<T>(bufpos<T, N>(N - k))] = mk<T>(s.x - wd.y, s.y + wd.x);
+        }
+    }
+    __syncthreads();
+    if constexpr (Plan<T, N>::S > 0) {
+        auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
+        auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
+        fft_inverse<T, N, NCOL, NT, false, true, true>(lds, lds, sts, sts, tw);
+        __syncthreads();
+    }
+    double tmax = 0;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int bad = 0;
+    const int nx = g.nx;
+    for (int e = threadIdx.x; e < ROWS * nx; e += NT) {
+        const int r = e / nx, i = e % nx;
+        const long long row = row0 + r;
+        if (row >= nrows) continue;
+        const int j = (int)(row % g.ny), k = (int)(row / g.ny);
+        const int pos = xpad<T>(i >> 1);
+        const C2<T> zx = sm[(0 * ROWS + r) * LP + pos];
+        const C2<T> zy = sm[(1 * ROWS + r) * LP + pos];
+        const C2<T> zz = sm[(2 * ROWS + r) * LP + pos];
+        const bool odd = i & 1;
+        const T hdx = (odd ? zx.y : zx.x) * scale;
+        const T hdy = (odd ? zy.y : zy.x) * scale;
+        const T hdz = (odd ? zz.y : zz.x) * scale;
+        cell_update<T>(g, P, io, M, Mn, Hout, row * nx + i, i, j, k, hdx, hdy, hdz, tmax, acc, bad);
+    }
+    block_finish<NT>(io, ctl, tmax, acc, bad);
+}
+
+// Demag-free step (terms.demag = false): H_eff from local terms only.
+template <class T>
+__global__ void __launch_bounds__(256)
+k_local_llg(Geo g, const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout, LocalParams<T> P,
+            StepIO io, Ctl ctl) {
+    if (halted(ctl)) return;
+    double tmax = 0;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int bad = 0;
+    const long long c = (long long)blockIdx.x * 256 + threadIdx.x;
+    if (c < g.ncell) {
+        const int i = (int)(c % g.nx);
+        const int j = (int)((c / g.nx) % g.ny);
+        const int k = (int)(c / ((long long)g.nx * g.ny));
+        cell_update<T>(g, P, io, M, Mn, Hout, c, i, j, k, T(0), T(0), T(0), tmax, acc, bad);
+    }
+    block_finish<256>(io, ctl, tmax, acc, bad);
+}
+
+} // namespace mfd
