@@ -131,6 +131,9 @@ mfd_status mfd_set_demag_octant_f64(mfd_ctx* ctx, const double* octant6);
 mfd_status mfd_get_demag_octant_f64(mfd_ctx* ctx, double* octant6);
 /* Read the real tensor spectrum octant as T widened to f64, layout [6][Py/2+1][Pz/2+1][Px/2+1]. */
 mfd_status mfd_get_spectrum_octant_f64(mfd_ctx* ctx, double* out);
+/* Run the pipeline up to pass `stage` (1..4) on the current M and copy the intermediate
+ * spectrum (1,4: [3][nz][ny][Hp]; 2,3: [3][nz][Py][Hp], Hp = pitch) as interleaved (re, im). */
+mfd_status mfd_debug_stage_f64(mfd_ctx* ctx, int stage, double* out);
 /* Device pointers of the resident state for zero-copy benchmarking:
  * m = current M (3 x N SoA of float or double). */
 mfd_status mfd_device_state(mfd_ctx* ctx, void** m, long long* ncell, int* precision_bits);

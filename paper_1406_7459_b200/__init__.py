@@ -114,6 +114,7 @@ def load_library() -> C.CDLL:
         "mfd_set_demag_octant_f64": (C.c_int, [V, _PD]),
         "mfd_get_demag_octant_f64": (C.c_int, [V, _PD]),
         "mfd_get_spectrum_octant_f64": (C.c_int, [V, _PD]),
+        "mfd_debug_stage_f64": (C.c_int, [V, C.c_int, _PD]),
         "mfd_device_state": (C.c_int, [V, C.POINTER(V), C.POINTER(C.c_longlong), C.POINTER(C.c_int)]),
         "mfd_launches_per_step": (C.c_int, [V]),
         "mfd_model_bytes_per_step": (C.c_double, [V]),
@@ -359,6 +360,15 @@ class Simulation:
         o = np.zeros((6, py // 2 + 1, pz // 2 + 1, px // 2 + 1))
         self._check(self.lib.mfd_get_spectrum_octant_f64(self.h, _ptr(o)))
         return o
+
+    def debug_stage(self, stage: int) -> np.ndarray:
+        """Intermediate spectrum after pass K<stage> (test hook), complex, pitch included."""
+        g = self.grid
+        hp = (padded_size(g.nx) // 2 + 1 + 15) // 16 * 16
+        rows = g.ny if stage in (1, 4) else padded_size(g.ny)
+        out = np.zeros(2 * 3 * g.nz * rows * hp)
+        self._check(self.lib.mfd_debug_stage_f64(self.h, stage, _ptr(out)))
+        return (out[0::2] + 1j * out[1::2]).reshape(3, g.nz, rows, hp)
 
     def device_state(self):
         p, n, prec = C.c_void_p(), C.c_longlong(), C.c_int()

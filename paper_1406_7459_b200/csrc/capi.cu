@@ -170,6 +170,9 @@ double mfd_stability_dt_limit(const mfd_material* m, const mfd_grid* g) {
 mfd_status mfd_set_demag_octant_f64(mfd_ctx* c, const double* o) { return guard(c, [&] { ENG(c)->set_octant(o); }); }
 mfd_status mfd_get_demag_octant_f64(mfd_ctx* c, double* o) { return guard(c, [&] { ENG(c)->get_octant(o); }); }
 mfd_status mfd_get_spectrum_octant_f64(mfd_ctx* c, double* o) { return guard(c, [&] { ENG(c)->get_spectrum(o); }); }
+mfd_status mfd_debug_stage_f64(mfd_ctx* c, int stage, double* out) {
+    return guard(c, [&] { ENG(c)->debug_stage(stage, out); });
+}
 mfd_status mfd_device_state(mfd_ctx* c, void** m, long long* n, int* prec) {
     return guard(c, [&] {
         *m = ENG(c)->state_ptr();

@@ -90,6 +90,7 @@ public:
     virtual void set_octant(const double*) = 0;
     virtual void get_octant(double*) = 0;
     virtual void get_spectrum(double*) = 0;
+    virtual void debug_stage(int stage, double* out) = 0;
     virtual void* state_ptr() = 0;
     virtual cudaStream_t stream() const = 0;
     virtual int launches_per_step() const = 0;
@@ -121,6 +122,7 @@ public:
     void set_octant(const double* oct) override;
     void get_octant(double* oct) override;
     void get_spectrum(double* out) override;
+    void debug_stage(int stage, double* out) override;
     void* state_ptr() override { return M_[cur_]; }
     cudaStream_t stream() const override { return stream_; }
     int launches_per_step() const override { return terms_.demag ? 5 : 1; }
@@ -166,6 +168,7 @@ private:
     int* h_err_ = nullptr;                     // pinned
     T* h_stage_ = nullptr;                     // pinned 3N staging
     long long k5_blocks_ = 1;
+    int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     static constexpr int kMaxChunk = 256;
 
     std::map<std::pair<std::vector<Iter>, int>, cudaGraphExec_t> graphs_;

@@ -109,7 +109,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         alloc(&A_, 3 * nrows * geo_.Hp * sizeof(C2<T>));
         alloc(&B_, 3 * (long long)g.nz * Py_ * geo_.Hp * sizeof(C2<T>));
         alloc(&Kt_, 6 * (long long)Hy_ * Hz_ * geo_.Hp * sizeof(T));
-        alloc(&ybuf_, Hy_ * sizeof(int));
+        alloc(&ybuf_, Py_ * sizeof(int));   // buffer row of every y frequency
         // twiddles exp(-2 pi i k / TWN), long double on the host, cast to T (fft.hpp:70-74)
         std::vector<C2<T>> tw(TWN);
         for (int k = 0; k < TWN; ++k) {
@@ -119,7 +119,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         }
         alloc(&tw_, TWN * sizeof(C2<T>));
         ck(cudaMemcpy(tw_, tw.data(), TWN * sizeof(C2<T>), cudaMemcpyHostToDevice), "tw upload");
-        k_ybuf<T><<<(Hy_ + 127) / 128, 128, 0, stream_>>>(Py_, Hy_, ybuf_);
+        k_ybuf<T><<<(Py_ + 127) / 128, 128, 0, stream_>>>(Py_, Py_, ybuf_);
         ck(cudaGetLastError(), "k_ybuf");
         // shared-memory opt-in for the instantiations this grid uses
         with_pow2(geo_.N, [&]<int L>() {
@@ -268,24 +268,28 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
         k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Mc, A_, tw_, ctl);
     });
     if (events) ck(cudaEventRecord(ev[1], stream_), "event");
+    if (stop_after_ == 1) return;
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         k_fft_y_fwd<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
     });
     if (events) ck(cudaEventRecord(ev[2], stream_), "event");
+    if (stop_after_ == 2) return;
     with_pow2(Pz_, [&]<int L>() {
         using CF = ZCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
         k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
     });
     if (events) ck(cudaEventRecord(ev[3], stream_), "event");
+    if (stop_after_ == 3) return;
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         k_fft_y_inv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
     });
     if (events) ck(cudaEventRecord(ev[4], stream_), "event");
+    if (stop_after_ == 4) return;
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
@@ -570,6 +574,34 @@ bool Engine<T>::relax(mfd_sample_cb cb, void* user) {
             cur_ ^= 1;
         }
         iter += K;
+    }
+}
+
+// Test hook: run the pipeline up to K<stage> on the current M and copy the
+// intermediate spectrum (A after K1/K4, B after K2/K3) out as interleaved
+// fp64 (re, im), pitch Hp included.
+template <class T>
+void Engine<T>::debug_stage(int stage, double* out) {
+    if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    if (stage < 1 || stage > 4) throw Error(MFD_EINVAL, "debug_stage: stage must be 1..4");
+    Iter it;
+    it.update = 0;
+    stop_after_ = stage;
+    try {
+        enqueue(it, cur_);
+    } catch (...) {
+        stop_after_ = 0;
+        throw;
+    }
+    stop_after_ = 0;
+    ck(cudaStreamSynchronize(stream_), "debug sync");
+    const bool isA = stage == 1 || stage == 4;
+    const long long cnt = isA ? 3LL * geo_.ny * geo_.nz * geo_.Hp : 3LL * geo_.nz * Py_ * geo_.Hp;
+    std::vector<C2<T>> h(cnt);
+    ck(cudaMemcpy(h.data(), isA ? A_ : B_, cnt * sizeof(C2<T>), cudaMemcpyDeviceToHost), "debug d2h");
+    for (long long i = 0; i < cnt; ++i) {
+        out[2 * i] = h[i].x;
+        out[2 * i + 1] = h[i].y;
     }
 }
 

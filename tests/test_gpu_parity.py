@@ -55,11 +55,16 @@ def test_device_tensor_vs_quad_truth(g):
     sim = engine_sim(s, 64)
     dev = sim.demag_octant()
     truth = O.tensor_octant(*g, which="quad")
+    # per entry: 1e-10 relative, or 5e-13 of the component's largest entry for the
+    # entries that nearly vanish by symmetry (where fp64 Newell cancels absolutely)
     for c in range(6):
         scale = np.max(np.abs(truth[c]))
+        if scale == 0:
+            assert np.all(dev[c] == 0)
+            continue
         err = np.abs(dev[c] - truth[c])
         rel = err / np.maximum(np.abs(truth[c]), 1e-300)
-        bad = (err > 5e-12 * np.abs(truth[c])) & (err > 1e-15 * scale)
+        bad = (err > 1e-10 * np.abs(truth[c])) & (err > 5e-13 * scale)
         assert not bad.any(), (c, float(rel[bad].max()), np.argwhere(bad)[:3])
 
 
