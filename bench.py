@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-step effective-field + LLG hot path (BASELINE.json).
+
+One "step" = Simulation<T>::step (sim.hpp:33-42): demag convolution (6 FFT
+passes + tensor product), exchange + anisotropy + Zeeman, LLG right-hand
+side, Euler update with |M| = Ms renormalisation and the max-torque
+reduction, on a grid of BASELINE.json's configs.
+
+Default workload (N=1): configs[3], the 512x512x64 thin film on which the
+north-star roofline target is quoted (>= 60% of HBM roofline per LLG step);
+fp32, cubic 2.5 nm cells, permalloy-like material with all four field terms
+active.  Synthetic data: uniform (1,1,1)/sqrt(3) start.
+
+Arms:
+  python bench.py [--gpus N --steps K --warmup W]     this engine (libmagfd_b200.so)
+  python bench.py --impl reference ...                 the reference CPU code (oracle/_ref)
+
+Multi-GPU (torchrun, N>1): round 1 runs one full replica per rank (weak
+scaling, no data-path collective); see DESIGN.md section "Multi-GPU".
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (nx, ny, nz, dx, dy, dz), BASELINE.json config string
+    "film512": ((512, 512, 64, 2.5e-9, 2.5e-9, 2.5e-9), "thin film 512x512x64 cells (BASELINE configs[3])"),
+    "sp4": ((128, 32, 1, 500e-9 / 128, 125e-9 / 32, 3e-9), "muMAG SP4 128x32x1 (configs[0])"),
+    "sp4fine": ((512, 128, 4, 500e-9 / 512, 125e-9 / 128, 0.75e-9), "SP4 refined 512x128x4 (configs[1])"),
+    "cube128": ((128, 128, 128, 2.5e-9, 2.5e-9, 2.5e-9), "permalloy cube 128^3 (configs[2])"),
+    "film1024": ((1024, 1024, 128, 2.5e-9, 2.5e-9, 2.5e-9), "large film 1024x1024x128 (configs[4])"),
+}
+MATERIAL = dict(A=1.3e-11, Ku=4e4, Ms=8e5, alpha=0.02, easy_axis=(0.0, 0.0, 1.0))
+H_EXT = (1e4, 0.0, 0.0)
+DT = 1e-14
+METRIC = "LLG cell-updates/s per step (N x steps/s) + % HBM roofline"
+UNIT = "cell-updates/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def model_bytes_per_kernel(g, s):
+    """Algorithmic HBM bytes of each pass (SURVEY.md section 8d, 5-pass model)."""
+    nx, ny, nz = g[:3]
+    N = nx * ny * nz
+    P = lambda n: 1 << (2 * n - 1).bit_length()
+    Px, Py, Pz = P(nx), P(ny), P(nz)
+    Hx = Px // 2 + 1
+    c = 2 * s
+    k1 = 3 * N * s + 3 * Hx * ny * nz * c
+    k2 = 3 * Hx * ny * nz * c + 3 * Hx * Py * nz * c
+    k3 = 2 * (3 * Hx * Py * nz * c) + 6 * Hx * (Py // 2 + 1) * (Pz // 2 + 1) * s
+    k4 = k2
+    k5 = 3 * Hx * ny * nz * c + 6 * N * s
+    return {"k_r2c_x": k1, "k_fft_y_fwd": k2, "k_fft_z_conv": k3, "k_fft_y_inv": k4, "k_c2r_x_llg": k5}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.idx = gpu_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.samples.append([v.strip() for v in line.split(",")])
+
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+                for n, v in zip(names, s[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except Exception:
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------- CPU reference
+def cpu_reference(steps, warmup, threads, sample_grid, precision=32, budget_s=None):
+    """Reference Simulation<T>::step (oracle/_ref, the unmodified reference code) on
+    the host cores.  Returns (cell-updates/s, ms/step, setup_s, steps_done)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref/libmagfd_ref.so not built")
+    g = sample_grid
+    spec = O.Spec(*g, **MATERIAL, h_ext=H_EXT, dt=DT, parallel=True, threads=threads)
+    t0 = time.perf_counter()
+    r = O.Ref(spec, precision)
+    n = spec.n
+    u = 1 / 3 ** 0.5
+    r.set_m(__import__("numpy").full((3, n), 8e5 * u))
+    setup = time.perf_counter() - t0
+    r.step(warmup)
+    times = []
+    for _ in range(steps):
+        t1 = time.perf_counter()
+        r.step(1)
+        times.append(time.perf_counter() - t1)
+        if budget_s and sum(times) > budget_s:
+            break
+    ms = statistics.median(times) * 1e3
+    return n / (ms / 1e3), ms, setup, len(times)
+
+
+def run_reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    g = WORKLOADS[args.workload][0]
+    sample = cpu_sample_grid(g)
+    try:
+        v, ms, setup, done = cpu_reference(args.steps, args.warmup, threads, sample, 32)
+    except Exception as e:  # reference not built on this box
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return
+    desc = (f"reference Simulation<float>::step (oracle/_ref, built from /root/reference/proj) on "
+            f"{sample[0]}x{sample[1]}x{sample[2]} cells (bounded sample of {g[0]}x{g[1]}x{g[2]}; same "
+            f"material, cell size, terms); {args.warmup} warm-up + median of {done} steps; setup {setup:.1f}s excluded")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
+                   "sample_grid": list(sample[:3]), "precision": "f32", "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def cpu_sample_grid(g):
+    """Bounded CPU sample: shrink x and y by 2 until <= 2.1M cells (keeps nz, cell size)."""
+    nx, ny, nz = g[:3]
+    while nx * ny * nz > 2_100_000 and nx > 8 and ny > 8:
+        nx //= 2
+        ny //= 2
+    return (nx, ny, nz) + tuple(g[3:])
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_1406_7459_b200 as E
+
+    torch.cuda.set_device(local)
+    g = WORKLOADS[args.workload][0]
+    prec = args.precision
+    s = 4 if prec == 32 else 8
+    grid = E.Grid(*g)
+    sim = E.Simulation(grid, E.Material(**MATERIAL), E.FieldConfig(True, True, True, True, H_EXT),
+                       E.StepperConfig(dt=DT), precision=prec, device=local,
+                       init_direction=(3 ** -0.5,) * 3)
+    stream = torch.cuda.ExternalStream(sim.stream_handle(), device=torch.device("cuda", local))
+    ncell = grid.cell_count
+
+    # warm-up (graph capture + clocks ramp)
+    sim.step_async(args.warmup)
+    sim.sync()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sim.step_async(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    sim.sync()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    ms_total = allmax(ws, e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    value = ws * ncell * args.steps / (ms_total / 1e3)
+
+    # per-kernel device time (events between passes, real steps on the same stream)
+    reps = max(5, min(20, args.steps))
+    acc = np.zeros(7)
+    for _ in range(reps):
+        acc += sim.step_timing()
+    per = acc / reps
+    names = ["k_r2c_x", "k_fft_y_fwd", "k_fft_z_conv", "k_fft_y_inv", "k_c2r_x_llg"]
+    per_kernel_ms = dict(zip(names, per[:5]))
+    mb = model_bytes_per_kernel(g, s)
+    top = max(per_kernel_ms, key=per_kernel_ms.get)
+    peak, peak_src = peaks()
+    achieved = mb[top] / (per_kernel_ms[top] / 1e3) / 1e9
+    step_bytes = sum(mb.values())
+
+    # e2e through the public API with pinned host buffers: per step H2D of M,
+    # Simulation::step, D2H of the step's torque.
+    e2e_steps = max(3, min(args.steps, 20))
+    host = torch.empty((3, ncell), dtype=torch.float32 if prec == 32 else torch.float64).pin_memory()
+    host_np = host.numpy()
+    host_np[:] = sim.get_m(dtype=np.float32 if prec == 32 else np.float64)
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sim.set_m(host_np)
+        torque = sim.step(1)
+    t_e2e = allmax(ws, time.perf_counter() - t0)
+    e2e_value = ws * ncell * e2e_steps / t_e2e
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload, {}).get(top)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.skip_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            sample = cpu_sample_grid(g)
+            v, cms, setup, done = cpu_reference(3, 1, threads, sample, prec, budget_s=25)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"reference Simulation<float>::step (oracle/_ref) on {sample[0]}x{sample[1]}x{sample[2]} "
+                             f"cells, same material/cell size/terms, {threads} host threads, 1 warm-up + median of "
+                             f"{done} steps ({cms:.0f} ms/step), setup {setup:.1f}s excluded"}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64",
+            "data": "synthetic (uniform (1,1,1)/sqrt3 start; random-free)",
+            "config": {"workload": WORKLOADS[args.workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
+                       "precision": "f32" if prec == 32 else "f64", "terms": "demag+exchange+anisotropy+zeeman",
+                       "parallelism": "replica per GPU" if ws > 1 else "1 GPU",
+                       "l2": "working set > 126 MB L2 (no flush needed)" if step_bytes > 4e8 else
+                             "working set fits L2 (inputs not flushed)"},
+            "steps_per_s": 1e3 / ms_step,
+            "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "model_bytes_per_launch": mb[top], "avg_launch_ms": per_kernel_ms[top]},
+            "step_roofline": {"model_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_step / 1e3) / 1e9,
+                              "frac": step_bytes / (ms_step / 1e3) / 1e9 / peak},
+            "per_kernel_ms": per_kernel_ms,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * ncell * s, "d2h_bytes_per_step": 8,
+                    "how": "per step: Simulation.set_m from pinned host M (C ABI mfd_set_m) + Simulation.step "
+                           "(mfd_step, returns the torque to the host)"},
+            "gpu_launches": sim.launches_per_step() * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="film512")
+    ap.add_argument("--precision", type=int, choices=[32, 64], default=32)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -136,7 +136,9 @@ private:
     double torque_of(unsigned long long bits) const;
     mfd_sample make_sample(const double sums[8], double torque) const;
     void eval(int write_h, bool sums, double& torque, double sum_out[8]);
-    void check_error_after(int n_done_on_error);
+    void ensure_stage() {
+        if (!h_stage_) ck(cudaMallocHost((void**)&h_stage_, 3 * geo_.ncell * sizeof(T)), "host alloc");
+    }
 
     mfd_grid grid_;
     mfd_material mat_;

@@ -102,7 +102,6 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     ck(cudaMallocHost((void**)&h_torque_, kMaxChunk * sizeof(unsigned long long)), "host alloc");
     ck(cudaMallocHost((void**)&h_sums_, kMaxChunk * 8 * sizeof(double)), "host alloc");
     ck(cudaMallocHost((void**)&h_err_, sizeof(int)), "host alloc");
-    ck(cudaMallocHost((void**)&h_stage_, 3 * n * sizeof(T)), "host alloc");
 
     if (terms_.demag) {
         const long long nrows = (long long)g.ny * g.nz;
@@ -345,9 +344,32 @@ double Engine<T>::torque_of(unsigned long long bits) const {
 }
 
 // --------------------------------------------------------------- state io
+// Same-precision transfers go straight from the caller's buffers (DMA at full
+// PCIe speed when they are pinned); cross-precision ones convert through the
+// pinned staging buffer.
+template <class T>
+static void copy3_h2d(T* dst, const T* x, const T* y, const T* z, long long n, cudaStream_t s) {
+    ck(cudaMemcpyAsync(dst, x, n * sizeof(T), cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(dst + n, y, n * sizeof(T), cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(dst + 2 * n, z, n * sizeof(T), cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaStreamSynchronize(s), "sync");
+}
+template <class T>
+static void copy3_d2h(const T* src, T* x, T* y, T* z, long long n, cudaStream_t s) {
+    ck(cudaMemcpyAsync(x, src, n * sizeof(T), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaMemcpyAsync(y, src + n, n * sizeof(T), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaMemcpyAsync(z, src + 2 * n, n * sizeof(T), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+}
+
 template <class T>
 void Engine<T>::set_m(const double* x, const double* y, const double* z) {
     const long long n = geo_.ncell;
+    if constexpr (std::is_same_v<T, double>) {
+        copy3_h2d<T>(M_[cur_], x, y, z, n, stream_);
+        return;
+    }
+    ensure_stage();
     for (long long i = 0; i < n; ++i) {
         h_stage_[i] = static_cast<T>(x[i]);
         h_stage_[i + n] = static_cast<T>(y[i]);
@@ -359,6 +381,11 @@ void Engine<T>::set_m(const double* x, const double* y, const double* z) {
 template <class T>
 void Engine<T>::set_m32(const float* x, const float* y, const float* z) {
     const long long n = geo_.ncell;
+    if constexpr (std::is_same_v<T, float>) {
+        copy3_h2d<T>(M_[cur_], x, y, z, n, stream_);
+        return;
+    }
+    ensure_stage();
     for (long long i = 0; i < n; ++i) {
         h_stage_[i] = static_cast<T>(x[i]);
         h_stage_[i + n] = static_cast<T>(y[i]);
@@ -370,6 +397,11 @@ void Engine<T>::set_m32(const float* x, const float* y, const float* z) {
 template <class T>
 void Engine<T>::get_m(double* x, double* y, double* z) {
     const long long n = geo_.ncell;
+    if constexpr (std::is_same_v<T, double>) {
+        copy3_d2h<T>(M_[cur_], x, y, z, n, stream_);
+        return;
+    }
+    ensure_stage();
     ck(cudaMemcpyAsync(h_stage_, M_[cur_], 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
     ck(cudaStreamSynchronize(stream_), "sync");
     for (long long i = 0; i < n; ++i) {
@@ -381,6 +413,11 @@ void Engine<T>::get_m(double* x, double* y, double* z) {
 template <class T>
 void Engine<T>::get_m32(float* x, float* y, float* z) {
     const long long n = geo_.ncell;
+    if constexpr (std::is_same_v<T, float>) {
+        copy3_d2h<T>(M_[cur_], x, y, z, n, stream_);
+        return;
+    }
+    ensure_stage();
     ck(cudaMemcpyAsync(h_stage_, M_[cur_], 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
     ck(cudaStreamSynchronize(stream_), "sync");
     for (long long i = 0; i < n; ++i) {
@@ -422,6 +459,7 @@ void Engine<T>::field(int which, double* x, double* y, double* z) {
     double tq;
     eval(which, false, tq, nullptr);
     const long long n = geo_.ncell;
+    ensure_stage();
     ck(cudaMemcpyAsync(h_stage_, H_, 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
     ck(cudaStreamSynchronize(stream_), "sync");
     for (long long i = 0; i < n; ++i) {
@@ -607,13 +645,21 @@ void Engine<T>::debug_stage(int stage, double* out) {
 
 template <class T>
 void Engine<T>::timing(double ms[7]) {
+    // One real Simulation::step with an event after every pass (advances the state).
     cudaEvent_t ev[6];
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
     Iter it;
-    it.update = 0;
-    it.renorm = 0;
+    it.update = 1;
+    it.renorm = ((stepno + 1) % st_.renorm_every) == 0;
+    ck(cudaMemsetAsync(torque_, 0, sizeof(unsigned long long), stream_), "memset");
     enqueue(it, cur_, true, ev);
-    ck(cudaStreamSynchronize(stream_), "sync");
+    std::vector<double> tq;
+    int err = 0;
+    fetch_chunk(1, tq, err);
+    if (err) throw Error(MFD_ENONFINITE, "eulerUpdate: non-finite magnetization after step (time step too large?)");
+    t += st_.dt;
+    stepno += 1;
+    cur_ ^= 1;
     for (int q = 0; q < 5; ++q) {
         float f = 0;
         cudaEventElapsedTime(&f, ev[q], ev[q + 1]);
