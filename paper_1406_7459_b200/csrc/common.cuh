@@ -121,22 +121,38 @@ constexpr int brev(int v, int bits) {
 // twiddles (1, -i) cost no multiply.
 // Decimation-in-frequency recursion on the sub-array v[OFF + k], k < R:
 // every index is a template constant, so the array never leaves registers.
-template <class T, int R, bool INV, int OFF>
+// ZIN: the upper half of the input is known to be zero (zero padding: every
+//      first forward stage, since n <= P/2), so the first level is a copy /
+//      twiddle only.
+// HOUT: only outputs k < R/2 are consumed (every last inverse stage: only
+//      the [0,n) corner is kept), so the final level skips the differences.
+//      Natural k < R/2 sit at even bit-reversed positions.
+template <class T, int R, bool INV, int OFF, bool ZIN = false, bool HOUT = false>
 struct DifStage {
     static __device__ __forceinline__ void run(C2<T>* v) {
         if constexpr (R > 1) {
             constexpr int H = R / 2;
             bfly<0>(v);
-            DifStage<T, H, INV, OFF>::run(v);
-            DifStage<T, H, INV, OFF + H>::run(v);
+            DifStage<T, H, INV, OFF, false, HOUT>::run(v);
+            DifStage<T, H, INV, OFF + H, false, HOUT>::run(v);
         }
     }
     template <int J>
     static __device__ __forceinline__ void bfly(C2<T>* v) {
         if constexpr (J < R / 2) {
-            const C2<T> a = v[OFF + J], b = v[OFF + J + R / 2];
-            v[OFF + J] = cadd<T>(a, b);
-            C2<T> d = csub<T>(a, b);
+            const C2<T> a = v[OFF + J];
+            if constexpr (HOUT && R == 2) {
+                v[OFF] = cadd<T>(a, v[OFF + 1]);
+                return;
+            }
+            C2<T> d;
+            if constexpr (ZIN) {
+                d = a;
+            } else {
+                const C2<T> b = v[OFF + J + R / 2];
+                v[OFF + J] = cadd<T>(a, b);
+                d = csub<T>(a, b);
+            }
             if constexpr (J == 0) {
             } else if constexpr (4 * J == R) {
                 d = cmul_mi<T, INV>(d);
@@ -162,10 +178,10 @@ __device__ __forceinline__ void unscramble(C2<T>* v) {
     }
 }
 
-template <class T, int R, bool INV>
+template <class T, int R, bool INV, bool ZIN = false, bool HOUT = false>
 __device__ __forceinline__ void dft(C2<T>* v) {
-    DifStage<T, R, INV, 0>::run(v);   // output in bit-reversed order
-    unscramble<T, R, 0>(v);           // compile-time register renaming
+    DifStage<T, R, INV, 0, ZIN && (R > 1), HOUT>::run(v);   // output in bit-reversed order
+    unscramble<T, R, 0>(v);                                  // compile-time register renaming
 }
 
 // Non-contracting arithmetic for the reference-order local-field / LLG code:

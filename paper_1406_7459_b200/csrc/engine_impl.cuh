@@ -124,13 +124,18 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         with_pow2(geo_.N, [&]<int L>() {
             set_smem<T>((const void*)k_r2c_x<T, L>, XCfg<T, L>::SMEM);
             set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM);
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
         });
         with_pow2(Py_, [&]<int L>() {
             set_smem<T>((const void*)k_fft_y_fwd<T, L>, YCfg<T, L>::SMEM);
             set_smem<T>((const void*)k_fft_y_inv<T, L>, YCfg<T, L>::SMEM);
         });
-        with_pow2(Pz_, [&]<int L>() { set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM); });
+        with_pow2(Pz_, [&]<int L>() {
+            if constexpr (z_variant<T, L>() == 2) set_smem<T>((const void*)k_fft_z_conv2<T, L>, Z2Cfg<T, L>::SMEM);
+            else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
+        });
         // tensor octant on the device (K0a), then spectra (K0b)
         alloc(&oct_, 6 * n * sizeof(double));
         launch_tensor_octant(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, oct_, stream_);
@@ -190,12 +195,13 @@ void Engine<T>::build_tensor_from_octant() {
         d.a_m = ny; d.a_k = 1; d.b_k = Hx; d.b_n = 1; d.o_m = Hx; d.o_n = 1;
         d.b_b1 = (long long)ny * Hx; d.o_b1 = (long long)Hy_ * Hx; d.nb2 = 1; d.scale = 1.0;
         launch_gemm64(d, nz, Cy[oy[c]], T1, T2, stream_);
-        // z: Kt[c][v][w][u] = s * sum_k Cz[w][k] T2[k][v][u];  two odd axes give (-2i)^2 = -4 -> s = -1
+        // z: Kt[v][w][u][c] = s * sum_k Cz[w][k] T2[k][v][u];  two odd axes give (-2i)^2 = -4 -> s = -1.
+        // The six components of a bin are interleaved so K3 reads them as three vectors.
         d = GemmDesc{};
         d.Mdim = Hz_; d.Ndim = Hx; d.Kdim = nz;
-        d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = Hp; d.o_n = 1;
-        d.b_b1 = Hx; d.o_b1 = (long long)Hz_ * Hp; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
-        launch_gemm64(d, Hy_, Cz[oz[c]], T2, Kt_ + (long long)c * Hy_ * Hz_ * Hp, stream_);
+        d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = 6LL * Hp; d.o_n = 6;
+        d.b_b1 = Hx; d.o_b1 = 6LL * Hz_ * Hp; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
+        launch_gemm64(d, Hy_, Cz[oz[c]], T2, Kt_ + c, stream_);
         ck(cudaGetLastError(), "tensor gemm");
     }
     ck(cudaStreamSynchronize(stream_), "tensor setup");
@@ -233,7 +239,7 @@ void Engine<T>::get_spectrum(double* out) {
             for (int w = 0; w < Hz_; ++w)
                 for (int u = 0; u < Hx; ++u)
                     out[(((long long)c * Hy_ + v) * Hz_ + w) * Hx + u] =
-                        (double)h[(((long long)c * Hy_ + v) * Hz_ + w) * geo_.Hp + u];
+                        (double)h[(((long long)v * Hz_ + w) * geo_.Hp + u) * 6 + c];
 }
 
 // --------------------------------------------------------------- enqueue
@@ -276,9 +282,18 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
     if (events) ck(cudaEventRecord(ev[2], stream_), "event");
     if (stop_after_ == 2) return;
     with_pow2(Pz_, [&]<int L>() {
-        using CF = ZCfg<T, L>;
-        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
-        k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+        if constexpr (z_variant<T, L>() == 1) {
+            dim3 grid((geo_.Hx + 31) / 32, Hy_, 1);
+            k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, B_, Kt_, ybuf_, ctl);
+        } else if constexpr (z_variant<T, L>() == 2) {
+            using CF = Z2Cfg<T, L>;
+            dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
+            k_fft_z_conv2<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+        } else {
+            using CF = ZCfg<T, L>;
+            dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
+            k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+        }
     });
     if (events) ck(cudaEventRecord(ev[3], stream_), "event");
     if (stop_after_ == 3) return;
@@ -292,7 +307,12 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
-        k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+        if (geo_.nx % V16<T>::V == 0 && io.sums)
+            k_c2r_x_llg_v<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+        else if (geo_.nx % V16<T>::V == 0)
+            k_c2r_x_llg_v<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+        else
+            k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
     });
     if (events) ck(cudaEventRecord(ev[5], stream_), "event");
 }

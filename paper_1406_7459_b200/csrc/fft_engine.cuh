@@ -91,8 +91,10 @@ __device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) 
 // tasks of one column (x pass: positions contiguous in HBM).
 // SYNC_MID inserts a barrier between the gather and scatter phases, required
 // when source and destination are the same shared buffer.
-template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, class LD,
-          class ST>
+// ZIN (first forward stage only): inputs n1 >= R/2 are zero padding, not loaded.
+// HOUT (last inverse stage only): outputs n1 >= R/2 are outside the kept corner.
+template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, bool ZIN = false,
+          bool HOUT = false, class LD, class ST>
 __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw) {
     using SI = StageInfo<T, L, s>;
     constexpr int R = SI::R, M = SI::M, MP = SI::MP;
@@ -113,7 +115,8 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
         n2v[i] = n2;
         if (TOTAL % NT == 0 || q < TOTAL) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) v[i][j] = ld(col, basev[i] + MP * j);
+            for (int j = 0; j < R; ++j)
+                v[i][j] = (ZIN && R > 1 && 2 * j >= R) ? mk<T>(0, 0) : ld(col, basev[i] + MP * j);
         }
     }
     if (SYNC_MID) __syncthreads();
@@ -122,7 +125,7 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
         const int q = threadIdx.x + i * NT;
         if (TOTAL % NT == 0 || q < TOTAL) {
             if (!INV) {
-                dft<T, R, false>(v[i]);
+                dft<T, R, false, ZIN>(v[i]);
                 if (MP > 1) {
 #pragma unroll
                     for (int k = 1; k < R; ++k) v[i][k] = cmul<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
@@ -132,10 +135,11 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
 #pragma unroll
                     for (int k = 1; k < R; ++k) v[i][k] = cmulc<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
                 }
-                dft<T, R, true>(v[i]);
+                dft<T, R, true, false, HOUT>(v[i]);
             }
 #pragma unroll
-            for (int j = 0; j < R; ++j) st(colv[i], basev[i] + MP * j, v[i][j]);
+            for (int j = 0; j < R; ++j)
+                if (!(HOUT && R > 1 && 2 * j >= R)) st(colv[i], basev[i] + MP * j, v[i][j]);
         }
     }
 }
@@ -145,19 +149,21 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
 // FIRST_SMEM / LAST_SMEM say whether ld0 / stN touch that same shared buffer,
 // in which case the stage gathers everything before a barrier and scatters
 // after it (in-place Stockham).  A barrier follows every shared-memory write.
-template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, class LD0,
-          class LDS, class STS, class STN>
+// PRUNE: the upper half of every input column is zero padding (n <= P/2 on
+// every axis), so the first stage skips those loads and the first DIF level.
+template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
+          class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM>(ld0, stn, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, PRUNE>(ld0, stn, tw);
     } else if constexpr (S == 2) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
     } else if constexpr (S == 3) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 1, false, NCOL, NT, COLFAST, true>(lds, sts, tw);
         __syncthreads();
@@ -167,23 +173,25 @@ __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN
 
 // Full inverse (transposed) transform: consumes buffer order via ld0,
 // produces natural order via stN.
-template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, class LD0,
-          class LDS, class STS, class STN>
+// PRUNE: only the lower half of every output column is kept (the [0,n)
+// corner), so the last stage skips the other half.
+template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
+          class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_inverse(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM>(ld0, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, false, PRUNE>(ld0, stn, tw);
     } else if constexpr (S == 2) {
         fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE>(lds, stn, tw);
     } else if constexpr (S == 3) {
         fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 1, true, NCOL, NT, COLFAST, true>(lds, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE>(lds, stn, tw);
     }
 }
 

@@ -11,7 +11,8 @@
 //   M      3 x N  SoA, x fastest (grid.hpp:30-34), double-buffered
 //   A      [3][nz][ny][Hp]  complex   x-spectrum of the active rows (Hp >= Px/2+1)
 //   B      [3][nz][Py][Hp]  complex   x,y-spectrum, y in buffer (digit-reversed) order
-//   Kt     [6][Py/2+1][Pz/2+1][Hp] T  real tensor spectrum octant (xx,yy,zz,xy,xz,yz)
+//   Kt     [Py/2+1][Pz/2+1][Hp][6] T  real tensor spectrum octant, components (xx,yy,zz,xy,xz,yz)
+//                                     interleaved per bin
 #pragma once
 #include "fft_engine.cuh"
 
@@ -223,15 +224,14 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
     fft_forward<T, L, NCOL, NT, true, false, true>(ld0, lds, sts, sts, tw);
     __syncthreads();
     // K~ . M~ : thread task (w, wq) covers z-frequencies {wq, Pz-wq} and both y rows.
-    const int Hy = Py / 2 + 1, Hz = L / 2 + 1;
-    const long long kcomp = (long long)Hy * Hz * Hp;
-    const T* kbase = Kt + ((long long)v * Hz) * Hp + u0;
+    const int Hz = L / 2 + 1;
+    const T* kbase = Kt + (((long long)v * Hz) * Hp + u0) * 6;
     for (int e = threadIdx.x; e < W * Hz; e += NT) {
         const int w = e % W, wq = e / W;
         if (u0 + w >= Hx) continue;
-        const T* kp = kbase + (long long)wq * Hp + w;
-        const T kxx = __ldg(kp), kyy = __ldg(kp + kcomp), kzz = __ldg(kp + 2 * kcomp);
-        const T kxy = __ldg(kp + 3 * kcomp), kxz = __ldg(kp + 4 * kcomp), kyz = __ldg(kp + 5 * kcomp);
+        const T* kp = kbase + ((long long)wq * Hp + w) * 6;
+        const T kxx = __ldg(kp), kyy = __ldg(kp + 1), kzz = __ldg(kp + 2);
+        const T kxy = __ldg(kp + 3), kxz = __ldg(kp + 4), kyz = __ldg(kp + 5);
         const int wpart = (L - wq) & (L - 1);
         const int nzf = wpart != wq ? 2 : 1;
         const int nr = pair ? 2 : 1;
@@ -252,6 +252,185 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
     }
     __syncthreads();
     fft_inverse<T, L, NCOL, NT, true, true, false>(lds, lds, sts, stn, tw);
+}
+
+// Tensor product at one z-frequency for the three components of one y row.
+// Kt octant entry at (u, v', w'); sy / sz are the mirror signs of the
+// partner row Py-v / partner plane Pz-w (odd components flip).
+// kp points at the bin's six interleaved components (Kt layout [v][w][u][6]),
+// read as three 8/16-byte vectors.
+template <class T>
+__device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* __restrict__ kp, T sy, T sz) {
+    const C2<T> k01 = __ldg(reinterpret_cast<const C2<T>*>(kp));
+    const C2<T> k23 = __ldg(reinterpret_cast<const C2<T>*>(kp) + 1);
+    const C2<T> k45 = __ldg(reinterpret_cast<const C2<T>*>(kp) + 2);
+    const T kxx = k01.x, kyy = k01.y, kzz = k23.x;
+    const T cxy = sy * k23.y, cxz = sz * k45.x;
+    const T cyz = sy * sz * k45.y;
+    const C2<T> a = mx, b = my, c = mz;
+    mx = mk<T>(kxx * a.x + cxy * b.x + cxz * c.x, kxx * a.y + cxy * b.y + cxz * c.y);
+    my = mk<T>(cxy * a.x + kyy * b.x + cyz * c.x, cxy * a.y + kyy * b.y + cyz * c.y);
+    mz = mk<T>(cxz * a.x + cyz * b.x + kzz * c.x, cxz * a.y + cyz * b.y + kzz * c.y);
+}
+
+// K3, two-stage plans (Pz = R0*R1).  Thread (x-bin w, stage-0 task n2, y-row
+// r) runs forward stage 0 for the three components with one set of twiddles
+// (HBM -> shared); then one thread per (w, k0, r) holds the three components
+// of its R1 frequencies f = k0 + R0*k1 in registers through forward stage 1,
+// the tensor product and the transposed inverse stage 1 (same positions), so
+// the product costs no extra shared-memory round trip; the inverse stage 0
+// goes shared -> HBM keeping the nz planes.
+template <class T, int L> struct Z2Cfg {
+    static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr int W = (sizeof(T) == 4 ? 16 : 8) / (R1 >= 16 ? 2 : 1);
+    static constexpr int NCOL = 6 * W;
+    static constexpr int NT = W * R1 * 2;
+    static constexpr int SMEM = NCOL * L * CS;
+};
+
+template <class T, int L>
+__global__ void __launch_bounds__(Z2Cfg<T, L>::NT)
+k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
+              const int* __restrict__ ybuf, Ctl ctl) {
+    using CF = Z2Cfg<T, L>;
+    constexpr int W = CF::W, NCOL = CF::NCOL, R0 = CF::R0, R1 = CF::R1;
+    static_assert(Plan<T, L>::S == 2 && R0 % R1 == 0, "two-stage plans with R0 % R1 == 0 only");
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const int u0 = blockIdx.x * W;
+    const int v = blockIdx.y;
+    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int vp = (Py - v) & (Py - 1);
+    const bool pair = vp != v;
+    const int w = threadIdx.x % W, n2 = (threadIdx.x / W) % R1, r = threadIdx.x / (W * R1);
+    const bool live = u0 + w < Hx && (pair || r == 0);
+    const long long cstride = (long long)nz * Py * Hp;
+    const long long kstride = (long long)Py * Hp;
+    C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Hp + u0 + w;   // + comp*cstride + k*kstride
+    // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
+    C2<T>* scol = sm + r * W + w;
+    // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding)
+    {
+    C2<T> twr[R0];
+#pragma unroll
+    for (int k = 1; k < R0; ++k) twr[k] = __ldg(tw + n2 * k * (TWN / L));
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        C2<T> x[R0];
+#pragma unroll
+        for (int j = 0; j < R0; ++j) {
+            const int pos = R1 * j + n2;
+            x[j] = (2 * j < R0 && live && pos < nz) ? gcol[c * cstride + pos * kstride] : mk<T>(0, 0);
+        }
+        dft<T, R0, false, true>(x);
+#pragma unroll
+        for (int k = 1; k < R0; ++k) x[k] = cmul<T>(x[k], twr[k]);
+#pragma unroll
+        for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * 2 * W] = x[k];
+    }
+    }
+    __syncthreads();
+    // ---- stage 1 + tensor product + inverse stage 1, in registers
+    const int Hz = L / 2 + 1;
+    const T sy = r ? T(-1) : T(1);
+#pragma unroll 1
+    for (int it = 0; it < R0 / R1; ++it) {
+        const int k0 = n2 + R1 * it;
+        C2<T> y[3][R1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int q = 0; q < R1; ++q) y[c][q] = scol[(k0 * R1 + q) * NCOL + c * 2 * W];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dft<T, R1, false>(y[c]);
+        if (live) {
+            const T* kb = Kt + ((long long)v * Hz * Hp + u0 + w) * 6;
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) {
+                const int f = k0 + R0 * k1;
+                const bool hi = 2 * f > L;
+                kmul<T>(y[0][k1], y[1][k1], y[2][k1], kb + (long long)(hi ? L - f : f) * Hp * 6, sy,
+                        hi ? T(-1) : T(1));
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dft<T, R1, true>(y[c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int q = 0; q < R1; ++q) scol[(k0 * R1 + q) * NCOL + c * 2 * W] = y[c][q];
+    }
+    __syncthreads();
+    // ---- inverse stage 0 (transposed): gather k0*R1 + n2, conj twiddle, IDFT, keep z < nz
+    C2<T> twr[R0];
+#pragma unroll
+    for (int k = 1; k < R0; ++k) twr[k] = __ldg(tw + n2 * k * (TWN / L));
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        C2<T> x[R0];
+#pragma unroll
+        for (int k = 0; k < R0; ++k) x[k] = scol[(k * R1 + n2) * NCOL + c * 2 * W];
+#pragma unroll
+        for (int k = 1; k < R0; ++k) x[k] = cmulc<T>(x[k], twr[k]);
+        dft<T, R0, true, false, true>(x);
+        if (live) {
+#pragma unroll
+            for (int j = 0; 2 * j < R0; ++j) {
+                const int pos = R1 * j + n2;
+                if (pos < nz) gcol[c * cstride + pos * kstride] = x[j];
+            }
+        }
+    }
+}
+
+// Which K3 variant a z length uses: 1 = all-register (L <= 16), 2 = two-stage
+// register product (fits shared memory), 0 = generic staged kernel.
+template <class T, int L>
+constexpr int z_variant() {
+    if constexpr (L <= 16 && Plan<T, L>::S <= 1) return 1;
+    else if constexpr (Plan<T, L>::S == 2 && Z2Cfg<T, L>::SMEM <= 200 * 1024 && Z2Cfg<T, L>::NT <= 1024) return 2;
+    else return 0;
+}
+
+// K3, single-stage plans (Pz <= 16): one thread per (x-bin, y-row) keeps the
+// three whole z-columns in registers; no shared memory, no barrier.
+template <class T, int L>
+__global__ void __launch_bounds__(64)
+k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int* __restrict__ ybuf, Ctl ctl) {
+    if (halted(ctl)) return;
+    const int w = threadIdx.x & 31, r = threadIdx.x >> 5;
+    const int u = blockIdx.x * 32 + w;
+    const int v = blockIdx.y;
+    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int vp = (Py - v) & (Py - 1);
+    if (u >= Hx || (r == 1 && vp == v)) return;
+    const long long row = r ? ybuf[vp] : ybuf[v];
+    const long long cstride = (long long)nz * Py * Hp, kstride = (long long)Py * Hp;
+    C2<T>* base = B + row * Hp + u;
+    C2<T> x[3][L];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < L; ++k) x[c][k] = (k < nz && 2 * k < L) ? base[c * cstride + k * kstride] : mk<T>(0, 0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dft<T, L, false, true>(x[c]);
+    const int Hz = L / 2 + 1;
+    const T* kb = Kt + ((long long)v * Hz * Hp + u) * 6;
+    const T sy = r ? T(-1) : T(1);
+#pragma unroll
+    for (int f = 0; f < L; ++f) {
+        const bool hi = 2 * f > L;
+        kmul<T>(x[0][f], x[1][f], x[2][f], kb + (long long)(hi ? L - f : f) * Hp * 6, sy, hi ? T(-1) : T(1));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dft<T, L, true, false, true>(x[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < L; ++k)
+            if (k < nz && 2 * k < L) base[c * cstride + k * kstride] = x[c][k];
 }
 
 // ------------------------------------------------------------------ K5
@@ -424,23 +603,17 @@ __device__ __forceinline__ void block_finish(const StepIO& io, const Ctl& ctl, d
     if (!last) return;
     __threadfence();
     const unsigned int total = gridDim.x * gridDim.y;
-    // fixed-order final combine: thread t sums partials t, t+NT, ... in order; then tree
-    __shared__ double fin[NT][7];
+    // fixed-order final combine by warp 0: lane l sums partials l, l+32, ... in
+    // order, then a fixed xor-shuffle tree — independent of scheduling.
+    if (wid != 0) return;
     for (int q = 0; q < 7; ++q) {
         double s = 0;
-        for (unsigned int b = threadIdx.x; b < total; b += NT) s += ((volatile double*)io.partials)[b * 8 + q];
-        fin[threadIdx.x][q] = s;
+        for (unsigned int b = lane; b < total; b += 32) s += ((volatile double*)io.partials)[b * 8 + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) io.sums_out[q] = s;
     }
-    __syncthreads();
-    for (int w = NT / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w)
-            for (int q = 0; q < 7; ++q) fin[threadIdx.x][q] += fin[threadIdx.x + w][q];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < 7; ++q) io.sums_out[q] = fin[0][q];
-        *io.ticket = 0;
-    }
+    if (lane == 0) *io.ticket = 0;
 }
 
 template <class T, int N>
@@ -506,6 +679,313 @@ k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __re
         const T hdy = (odd ? zy.y : zy.x) * scale;
         const T hdz = (odd ? zz.y : zz.x) * scale;
         cell_update<T>(g, P, io, M, Mn, Hout, row * nx + i, i, j, k, hdx, hdy, hdz, tmax, acc, bad);
+    }
+    block_finish<NT>(io, ctl, tmax, acc, bad);
+}
+
+// Per-cell H_eff + LLG + Euler from register values, reference operation
+// order (identical arithmetic to cell_update).  nb: neighbours x-, x+, y-,
+// y+, z-, z+ (only read where has[] is set, Neumann boundaries).
+template <class T>
+__device__ __forceinline__ void cell_core(const LocalParams<T>& P, const StepIO& io, T mx, T my, T mz,
+                                          const T (&nb)[6][3], const bool (&has)[6], T hdx, T hdy, T hdz,
+                                          T (&mo)[3], T (&ho)[3], double& tmax, double* acc, int& bad,
+                                          bool& write) {
+    T Hx = hdx, Hy = hdy, Hz = hdz;
+    double elink = 0;
+    if (P.exch) {
+        T h0 = 0, h1 = 0, h2 = 0;
+        const T wv[6] = {P.cx, P.cx, P.cy, P.cy, P.cz, P.cz};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            if (has[q]) {
+                h0 = add_rn(h0, mul_rn(wv[q], sub_rn(nb[q][0], mx)));
+                h1 = add_rn(h1, mul_rn(wv[q], sub_rn(nb[q][1], my)));
+                h2 = add_rn(h2, mul_rn(wv[q], sub_rn(nb[q][2], mz)));
+            }
+        }
+        if (io.sums) {
+            const double ww[3] = {P.wx, P.wy, P.wz};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (has[2 * a + 1]) {
+                    const double e0 = (double)nb[2 * a + 1][0] - mx, e1 = (double)nb[2 * a + 1][1] - my,
+                                 e2 = (double)nb[2 * a + 1][2] - mz;
+                    elink += ww[a] * (e0 * e0 + e1 * e1 + e2 * e2);
+                }
+            }
+        }
+        Hx = add_rn(Hx, h0);
+        Hy = add_rn(Hy, h1);
+        Hz = add_rn(Hz, h2);
+    }
+    if (P.anis) {
+        const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
+        Hx = add_rn(Hx, mul_rn(proj, P.ax));
+        Hy = add_rn(Hy, mul_rn(proj, P.ay));
+        Hz = add_rn(Hz, mul_rn(proj, P.az));
+    }
+    if (P.zee) {
+        Hx = add_rn(Hx, P.hx);
+        Hy = add_rn(Hy, P.hy);
+        Hz = add_rn(Hz, P.hz);
+    }
+    if (io.write_h == 1) {
+        ho[0] = Hx; ho[1] = Hy; ho[2] = Hz;
+    } else {
+        ho[0] = hdx; ho[1] = hdy; ho[2] = hdz;
+    }
+    if (io.sums) {
+        acc[0] += (double)mx;
+        acc[1] += (double)my;
+        acc[2] += (double)mz;
+        acc[3] += elink;
+        const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
+        const double p = m0 * P.dax + m1 * P.day + m2 * P.daz;
+        acc[4] += 1.0 - p * p;
+        acc[5] += (double)hdx * mx + (double)hdy * my + (double)hdz * mz;
+        acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
+    }
+    const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
+    const T c0 = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
+    const T c1 = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
+    const T c2 = sub_rn(mul_rn(mx, b1), mul_rn(my, b0));
+    const T d0 = sub_rn(mul_rn(my, c2), mul_rn(mz, c1));
+    const T d1 = sub_rn(mul_rn(mz, c0), mul_rn(mx, c2));
+    const T d2 = sub_rn(mul_rn(mx, c1), mul_rn(my, c0));
+    const T r0 = add_rn(mul_rn(P.precess, c0), mul_rn(P.damp, d0));
+    const T r1 = add_rn(mul_rn(P.precess, c1), mul_rn(P.damp, d1));
+    const T r2 = add_rn(mul_rn(P.precess, c2), mul_rn(P.damp, d2));
+    {
+        const double v0 = r0, v1 = r1, v2 = r2;
+        tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
+    }
+    write = false;
+    if (io.update) {
+        T e0 = add_rn(mx, mul_rn(P.dt, r0));
+        T e1 = add_rn(my, mul_rn(P.dt, r1));
+        T e2 = add_rn(mz, mul_rn(P.dt, r2));
+        if (io.renorm) {
+            const T n2 = add_rn(add_rn(mul_rn(e0, e0), mul_rn(e1, e1)), mul_rn(e2, e2));
+            if (!(n2 > T(0)) || !isfinite((double)n2)) { bad = 1; return; }
+            const T f = P.Ms / sqrt(n2);
+            e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
+        } else if (!isfinite((double)add_rn(add_rn(e0, e1), e2))) {
+            bad = 1;
+            return;
+        }
+        mo[0] = e0; mo[1] = e1; mo[2] = e2;
+        write = true;
+    }
+}
+
+// 16-byte vector of V = 16/sizeof(T) consecutive cells.
+template <class T> struct V16;
+template <> struct V16<float> { using type = float4; static constexpr int V = 4; };
+template <> struct V16<double> { using type = double2; static constexpr int V = 2; };
+
+template <class T>
+__device__ __forceinline__ void vload(const T* p, T* out) {
+    using VT = typename V16<T>::type;
+    const VT v = __ldg(reinterpret_cast<const VT*>(p));
+    if constexpr (V16<T>::V == 4) { out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w; }
+    else { out[0] = v.x; out[1] = v.y; }
+}
+template <class T>
+__device__ __forceinline__ void vstore(T* p, const T* in) {
+    using VT = typename V16<T>::type;
+    VT v;
+    if constexpr (V16<T>::V == 4) { v.x = in[0]; v.y = in[1]; v.z = in[2]; v.w = in[3]; }
+    else { v.x = in[0]; v.y = in[1]; }
+    *reinterpret_cast<VT*>(p) = v;
+}
+
+// Vectorised epilogue over V cells [i0, i0+V) of one row: M, its six
+// neighbours and the results move as 16-byte vectors.  Requires nx % V == 0.
+// The exchange field of component c needs only component c of the
+// neighbours, so the stencil runs one component at a time (register use
+// independent of the component count); per cell and component the sum is
+// accumulated in the reference order x-, x+, y-, y+, z-, z+ (fields.hpp:33-48).
+template <class T, bool SUMS>
+__device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
+                                          const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
+                                          long long c0, int i0, int j, int k, const T (&hd)[3][V16<T>::V],
+                                          double& tmax, double* acc, int& bad) {
+    constexpr int V = V16<T>::V;
+    const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
+    const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = k > 0, hz1 = k < g.nz - 1;
+    const bool hx0 = i0 > 0, hx1 = i0 + V < g.nx;
+    T m[3][V], H[3][V];
+    double elink[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) elink[q] = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const T* p = M + c * n + c0;
+        vload<T>(p, m[c]);
+        if (!P.exch) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) H[c][q] = hd[c][q];
+            continue;
+        }
+        T ym[V], yp[V], zm[V], zp[V];
+        if (hy0) vload<T>(p - sy, ym);
+        if (hy1) vload<T>(p + sy, yp);
+        if (hz0) vload<T>(p - sz, zm);
+        if (hz1) vload<T>(p + sz, zp);
+        const T xl = hx0 ? __ldg(p - 1) : T(0);
+        const T xr = hx1 ? __ldg(p + V) : T(0);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const T mc = m[c][q];
+            const T xm = q > 0 ? m[c][q - 1] : xl, xp = q < V - 1 ? m[c][q + 1] : xr;
+            T h = 0;
+            if (q > 0 || hx0) h = add_rn(h, mul_rn(P.cx, sub_rn(xm, mc)));
+            if (q < V - 1 || hx1) h = add_rn(h, mul_rn(P.cx, sub_rn(xp, mc)));
+            if (hy0) h = add_rn(h, mul_rn(P.cy, sub_rn(ym[q], mc)));
+            if (hy1) h = add_rn(h, mul_rn(P.cy, sub_rn(yp[q], mc)));
+            if (hz0) h = add_rn(h, mul_rn(P.cz, sub_rn(zm[q], mc)));
+            if (hz1) h = add_rn(h, mul_rn(P.cz, sub_rn(zp[q], mc)));
+            H[c][q] = add_rn(hd[c][q], h);
+            if (SUMS) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
+                if (q < V - 1 || hx1) { const double e = (double)xp - mc; elink[q] += P.wx * e * e; }
+                if (hy1) { const double e = (double)yp[q] - mc; elink[q] += P.wy * e * e; }
+                if (hz1) { const double e = (double)zp[q] - mc; elink[q] += P.wz * e * e; }
+            }
+        }
+    }
+    T mo[3][V];
+    bool all = true;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+        const T mx = m[0][q], my = m[1][q], mz = m[2][q];
+        T Hx = H[0][q], Hy = H[1][q], Hz = H[2][q];
+        if (P.anis) {
+            const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
+            Hx = add_rn(Hx, mul_rn(proj, P.ax));
+            Hy = add_rn(Hy, mul_rn(proj, P.ay));
+            Hz = add_rn(Hz, mul_rn(proj, P.az));
+        }
+        if (P.zee) {
+            Hx = add_rn(Hx, P.hx);
+            Hy = add_rn(Hy, P.hy);
+            Hz = add_rn(Hz, P.hz);
+        }
+        if (io.write_h == 1) { H[0][q] = Hx; H[1][q] = Hy; H[2][q] = Hz; }
+        if (SUMS) {
+            acc[0] += (double)mx;
+            acc[1] += (double)my;
+            acc[2] += (double)mz;
+            acc[3] += elink[q];
+            const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
+            const double pp = m0 * P.dax + m1 * P.day + m2 * P.daz;
+            acc[4] += 1.0 - pp * pp;
+            acc[5] += (double)hd[0][q] * mx + (double)hd[1][q] * my + (double)hd[2][q] * mz;
+            acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
+        }
+        const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
+        const T c0x = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
+        const T c1x = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
+        const T c2x = sub_rn(mul_rn(mx, b1), mul_rn(my, b0));
+        const T d0 = sub_rn(mul_rn(my, c2x), mul_rn(mz, c1x));
+        const T d1 = sub_rn(mul_rn(mz, c0x), mul_rn(mx, c2x));
+        const T d2 = sub_rn(mul_rn(mx, c1x), mul_rn(my, c0x));
+        const T r0 = add_rn(mul_rn(P.precess, c0x), mul_rn(P.damp, d0));
+        const T r1 = add_rn(mul_rn(P.precess, c1x), mul_rn(P.damp, d1));
+        const T r2 = add_rn(mul_rn(P.precess, c2x), mul_rn(P.damp, d2));
+        {
+            const double v0 = r0, v1 = r1, v2 = r2;
+            tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
+        }
+        T e0 = add_rn(mx, mul_rn(P.dt, r0));
+        T e1 = add_rn(my, mul_rn(P.dt, r1));
+        T e2 = add_rn(mz, mul_rn(P.dt, r2));
+        if (io.renorm) {
+            const T n2 = add_rn(add_rn(mul_rn(e0, e0), mul_rn(e1, e1)), mul_rn(e2, e2));
+            if (!(n2 > T(0)) || !isfinite((double)n2)) {
+                all = false;
+            } else {
+                const T f = P.Ms / sqrt(n2);
+                e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
+            }
+        } else if (!isfinite((double)add_rn(add_rn(e0, e1), e2))) {
+            all = false;
+        }
+        mo[0][q] = e0; mo[1][q] = e1; mo[2][q] = e2;
+    }
+    if (io.write_h) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vstore<T>(Hout + c * n + c0, io.write_h == 1 ? H[c] : hd[c]);
+    }
+    if (io.update) {
+        if (!all) bad = 1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vstore<T>(Mn + c * n + c0, mo[c]);
+    }
+}
+
+template <class T, int N, bool SUMS>
+__global__ void __launch_bounds__(LCfg<T, N>::NT)
+k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
+              T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl) {
+    using CF = LCfg<T, N>;
+    constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
+    constexpr int V = V16<T>::V;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    const long long nrows = (long long)g.ny * g.nz;
+    const long long row0 = (long long)blockIdx.x * ROWS;
+    constexpr int HALF = N / 2 + 1;
+    for (int e = threadIdx.x; e < NCOL * HALF; e += NT) {
+        const int col = e / HALF, k = e % HALF;
+        const int comp = col / ROWS, r = col % ROWS;
+        const long long row = row0 + r;
+        C2<T> a = mk<T>(0, 0), b = mk<T>(0, 0);
+        if (row < nrows) {
+            const C2<T>* src = A + ((long long)comp * nrows + row) * g.Hp;
+            a = src[k];
+            b = src[N - k];
+        }
+        const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));
+        {
+            const C2<T> s = cadd<T>(a, cconj<T>(b)), d = csub<T>(a, cconj<T>(b));
+            const C2<T> wd = cmulc<T>(d, w);
+            sm[col * LP + xpad<T>(bufpos<T, N>(k % N))] = mk<T>(s.x - wd.y, s.y + wd.x);
+        }
+        if (N - k != k && N - k < N) {
+            const C2<T> s = cadd<T>(b, cconj<T>(a)), d = csub<T>(b, cconj<T>(a));
+            const C2<T> wn = mk<T>(-w.x, w.y);
+            const C2<T> wd = cmulc<T>(d, wn);
+            sm[col * LP + xpad<T>(bufpos<T, N>(N - k))] = mk<T>(s.x - wd.y, s.y + wd.x);
+        }
+    }
+    __syncthreads();
+    if constexpr (Plan<T, N>::S > 0) {
+        auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
+        auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
+        fft_inverse<T, N, NCOL, NT, false, true, true>(lds, lds, sts, sts, tw);
+        __syncthreads();
+    }
+    double tmax = 0;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int bad = 0;
+    const int nx = g.nx, nvec = nx / V;
+    for (int e = threadIdx.x; e < ROWS * nvec; e += NT) {
+        const int r = e / nvec, i0 = (e % nvec) * V;
+        const long long row = row0 + r;
+        if (row >= nrows) continue;
+        const int j = (int)(row % g.ny), k = (int)(row / g.ny);
+        T hd[3][V];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int q = 0; q < V; q += 2) {
+                const C2<T> z = sm[(c * ROWS + r) * LP + xpad<T>((i0 + q) >> 1)];
+                hd[c][q] = z.x * scale;
+                hd[c][q + 1] = z.y * scale;
+            }
+        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, row * nx + i0, i0, j, k, hd, tmax, acc, bad);
     }
     block_finish<NT>(io, ctl, tmax, acc, bad);
 }
