@@ -76,6 +76,16 @@ __device__ __forceinline__ int bufpos(int f) {
     }
 }
 
+// Natural frequency of output k of last-stage task p (the last stage has
+// MP = 1): f = k0 + R0*k1 + R0*R1*k2 with the leading digits encoded in p.
+template <class T, int L>
+__device__ __forceinline__ int natfreq(int p, int k) {
+    using P = Plan<T, L>;
+    if constexpr (P::S <= 1) return k;
+    else if constexpr (P::S == 2) return p + P::R0 * k;
+    else return (p / P::R1) + P::R0 * (p % P::R1) + P::R0 * P::R1 * k;
+}
+
 // Twiddle W_M^{e} (forward sign) from the global table of TWN entries.
 constexpr int TWN = 4096;
 template <class T, int M>
@@ -94,15 +104,18 @@ __device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) 
 // ZIN (first forward stage only): inputs n1 >= R/2 are zero padding, not loaded.
 // HOUT (last inverse stage only): outputs n1 >= R/2 are outside the kept corner.
 template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, bool ZIN = false,
-          bool HOUT = false, class LD, class ST>
+          bool HOUT = false, bool NAT = false, class LD, class ST>
 __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw) {
     using SI = StageInfo<T, L, s>;
     constexpr int R = SI::R, M = SI::M, MP = SI::MP;
     constexpr int TPC = L / R;
     constexpr int TOTAL = NCOL * TPC;
     constexpr int TPT = (TOTAL + NT - 1) / NT;
+    // NAT on the last stage: the frequency side (forward output / inverse
+    // input) uses natural order instead of buffer order.
+    constexpr bool NATF = NAT && s == Plan<T, L>::S - 1;
     C2<T> v[TPT][R];
-    int colv[TPT], basev[TPT], n2v[TPT];
+    int colv[TPT], basev[TPT], n2v[TPT], pv[TPT];
 #pragma unroll
     for (int i = 0; i < TPT; ++i) {
         const int q = threadIdx.x + i * NT;
@@ -113,10 +126,13 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
         colv[i] = col;
         basev[i] = p * M + n2;
         n2v[i] = n2;
+        pv[i] = p;
         if (TOTAL % NT == 0 || q < TOTAL) {
 #pragma unroll
             for (int j = 0; j < R; ++j)
-                v[i][j] = (ZIN && R > 1 && 2 * j >= R) ? mk<T>(0, 0) : ld(col, basev[i] + MP * j);
+                v[i][j] = (ZIN && R > 1 && 2 * j >= R)
+                              ? mk<T>(0, 0)
+                              : ld(col, (NATF && INV) ? natfreq<T, L>(p, j) : basev[i] + MP * j);
         }
     }
     if (SYNC_MID) __syncthreads();
@@ -139,7 +155,8 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
             }
 #pragma unroll
             for (int j = 0; j < R; ++j)
-                if (!(HOUT && R > 1 && 2 * j >= R)) st(colv[i], basev[i] + MP * j, v[i][j]);
+                if (!(HOUT && R > 1 && 2 * j >= R))
+                    st(colv[i], (NATF && !INV) ? natfreq<T, L>(pv[i], j) : basev[i] + MP * j, v[i][j]);
         }
     }
 }
@@ -151,23 +168,24 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
 // after it (in-place Stockham).  A barrier follows every shared-memory write.
 // PRUNE: the upper half of every input column is zero padding (n <= P/2 on
 // every axis), so the first stage skips those loads and the first DIF level.
+// NAT: the last stage writes natural frequency order (instead of buffer order).
 template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
-          class LD0, class LDS, class STS, class STN>
+          bool NAT = false, class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, PRUNE>(ld0, stn, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, PRUNE, false, NAT>(ld0, stn, tw);
     } else if constexpr (S == 2) {
         fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT>(lds, stn, tw);
     } else if constexpr (S == 3) {
         fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 1, false, NCOL, NT, COLFAST, true>(lds, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 2, false, NCOL, NT, COLFAST, LAST_SMEM>(lds, stn, tw);
+        fft_stage<T, L, 2, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT>(lds, stn, tw);
     }
 }
 
@@ -175,19 +193,20 @@ __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN
 // produces natural order via stN.
 // PRUNE: only the lower half of every output column is kept (the [0,n)
 // corner), so the last stage skips the other half.
+// NAT: the first stage reads natural frequency order (instead of buffer order).
 template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
-          class LD0, class LDS, class STS, class STN>
+          bool NAT = false, class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_inverse(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, false, PRUNE>(ld0, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, false, PRUNE, NAT>(ld0, stn, tw);
     } else if constexpr (S == 2) {
-        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE>(lds, stn, tw);
     } else if constexpr (S == 3) {
-        fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM>(ld0, sts, tw);
+        fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT>(ld0, sts, tw);
         __syncthreads();
         fft_stage<T, L, 1, true, NCOL, NT, COLFAST, true>(lds, sts, tw);
         __syncthreads();

@@ -41,7 +41,7 @@ template <class T, int N> struct LCfg {   // K5
 };
 template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int CS = sizeof(C2<T>);
-    static constexpr int W = cmax(1, cmin(128 / CS, 131072 / (L * CS)));
+    static constexpr int W = cmax(1, cmin(128 / CS, 65536 / (L * CS)));   // <= 64 KB tile: 2+ CTAs/SM
     static constexpr int NT = clampNT(W * L / regE<T>());
     static constexpr int SMEM = Plan<T, L>::S >= 2 ? W * L * CS : 0;
 };
@@ -110,25 +110,31 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
     if constexpr (Plan<T, N>::S == 0) {
         for (int c = threadIdx.x; c < ROWS; c += NT) sts(c, 0, ld0(c, 0));
     } else {
-        fft_forward<T, N, ROWS, NT, false, false, true>(ld0, lds, sts, sts, tw);
+        // last stage writes natural frequency order: the post-process needs no index reversal
+        fft_forward<T, N, ROWS, NT, false, false, true, true, true>(ld0, lds, sts, sts, tw);
     }
     __syncthreads();
-    // Real-to-complex post-process: X[k] = E + W^k O, X[N-k] = conj(E - W^k O).
-    constexpr int HALF = N / 2 + 1;
-    for (int e = threadIdx.x; e < ROWS * HALF; e += NT) {
-        const int col = e / HALF, k = e % HALF;
-        const long long row = row0 + col;
-        if (row >= nrows) continue;
-        const C2<T> zk = sm[col * LP + xpad<T>(bufpos<T, N>(k % N))];
-        const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>(bufpos<T, N>((N - k) % N))]);
+    // Real-to-complex post-process on pairs (k, N-k): X[k] = E + W^k O,
+    // X[N-k] = conj(E - W^k O).  Item e -> (k = e % (N/2), row = e / (N/2));
+    // the k = 0 item also emits the self-paired k = N/2.
+    auto post = [&](int col, int k) {
+        const C2<T> zk = sm[col * LP + xpad<T>(k & (N - 1))];
+        const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>((N - k) & (N - 1))]);
         const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
         const C2<T> d = csub<T>(zk, zn);
         const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
         const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));        // W_Px^k
         const C2<T> wo = cmul<T>(w, O);
-        C2<T>* dst = A + ((long long)comp * nrows + row) * g.Hp;
+        C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
         dst[k] = cadd<T>(E, wo);
         if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
+    };
+    constexpr int HP = N / 2 > 0 ? N / 2 : 1;
+    for (int e = threadIdx.x; e < ROWS * HP; e += NT) {
+        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+        if (row0 + col >= nrows) continue;
+        post(col, k);
+        if (k == 0 && N > 1) post(col, N / 2);
     }
 }
 
@@ -311,8 +317,20 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Hp + u0 + w;   // + comp*cstride + k*kstride
     // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + r * W + w;
-    // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding)
+    // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
+    // All 3*R0/2 HBM loads of the thread are issued before any arithmetic.
     {
+    // software pipeline over the three components: the loads of component
+    // c+1 are in flight while component c is transformed.
+    C2<T> nxt[R0 / 2];
+    auto fetch = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < R0 / 2; ++j) {
+            const int pos = R1 * j + n2;
+            nxt[j] = (live && pos < nz) ? gcol[c * cstride + pos * kstride] : mk<T>(0, 0);
+        }
+    };
+    fetch(0);
     C2<T> twr[R0];
 #pragma unroll
     for (int k = 1; k < R0; ++k) twr[k] = __ldg(tw + n2 * k * (TWN / L));
@@ -320,10 +338,8 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     for (int c = 0; c < 3; ++c) {
         C2<T> x[R0];
 #pragma unroll
-        for (int j = 0; j < R0; ++j) {
-            const int pos = R1 * j + n2;
-            x[j] = (2 * j < R0 && live && pos < nz) ? gcol[c * cstride + pos * kstride] : mk<T>(0, 0);
-        }
+        for (int j = 0; j < R0; ++j) x[j] = 2 * j < R0 ? nxt[j] : mk<T>(0, 0);
+        if (c < 2) fetch(c + 1);
         dft<T, R0, false, true>(x);
 #pragma unroll
         for (int k = 1; k < R0; ++k) x[k] = cmul<T>(x[k], twr[k]);
@@ -936,42 +952,66 @@ k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const long long nrows = (long long)g.ny * g.nz;
     const long long row0 = (long long)blockIdx.x * ROWS;
-    constexpr int HALF = N / 2 + 1;
-    for (int e = threadIdx.x; e < NCOL * HALF; e += NT) {
-        const int col = e / HALF, k = e % HALF;
-        const int comp = col / ROWS, r = col % ROWS;
-        const long long row = row0 + r;
-        C2<T> a = mk<T>(0, 0), b = mk<T>(0, 0);
-        if (row < nrows) {
-            const C2<T>* src = A + ((long long)comp * nrows + row) * g.Hp;
-            a = src[k];
-            b = src[N - k];
+    // C2R pre-process over pairs (k, N-k): item e -> (k = e % (N/2), column
+    // = e / (N/2)); the k = 0 item also carries the self-paired k = N/2.  All
+    // HBM loads of the thread are issued before any use (compile-time trip
+    // count) so the latency is paid once.  Z is written in natural order; the
+    // first inverse stage reads natural order.
+    constexpr int HP = N / 2 > 0 ? N / 2 : 1;
+    constexpr int ITEMS = NCOL * HP;
+    constexpr int IT = (ITEMS + NT - 1) / NT;
+    C2<T> pa[IT], pb[IT], pc[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const int e = threadIdx.x + it * NT;
+        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+        const long long row = row0 + col % ROWS;
+        pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
+        if (e < ITEMS && row < nrows) {
+            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
+            pa[it] = src[k];
+            pb[it] = src[N - k];
+            if (k == 0 && N > 1) pc[it] = src[N / 2];
         }
+    }
+    auto pre = [&](C2<T>* scol, int k, C2<T> a, C2<T> b) {
         const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));
         {
             const C2<T> s = cadd<T>(a, cconj<T>(b)), d = csub<T>(a, cconj<T>(b));
             const C2<T> wd = cmulc<T>(d, w);
-            sm[col * LP + xpad<T>(bufpos<T, N>(k % N))] = mk<T>(s.x - wd.y, s.y + wd.x);
+            scol[xpad<T>(k & (N - 1))] = mk<T>(s.x - wd.y, s.y + wd.x);
         }
         if (N - k != k && N - k < N) {
             const C2<T> s = cadd<T>(b, cconj<T>(a)), d = csub<T>(b, cconj<T>(a));
             const C2<T> wn = mk<T>(-w.x, w.y);
             const C2<T> wd = cmulc<T>(d, wn);
-            sm[col * LP + xpad<T>(bufpos<T, N>(N - k))] = mk<T>(s.x - wd.y, s.y + wd.x);
+            scol[xpad<T>(N - k)] = mk<T>(s.x - wd.y, s.y + wd.x);
         }
+    };
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const int e = threadIdx.x + it * NT;
+        if (ITEMS % NT != 0 && e >= ITEMS) continue;
+        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+        pre(sm + col * LP, k, pa[it], pb[it]);
+        if (k == 0 && N > 1) pre(sm + col * LP, N / 2, pc[it], pc[it]);
     }
     __syncthreads();
     if constexpr (Plan<T, N>::S > 0) {
         auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
         auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
-        fft_inverse<T, N, NCOL, NT, false, true, true>(lds, lds, sts, sts, tw);
+        fft_inverse<T, N, NCOL, NT, false, true, true, true, true>(lds, lds, sts, sts, tw);
         __syncthreads();
     }
     double tmax = 0;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
     int bad = 0;
     const int nx = g.nx, nvec = nx / V;
-    for (int e = threadIdx.x; e < ROWS * nvec; e += NT) {
+    constexpr int EIT = (ROWS * (N / V) + NT - 1) / NT;   // nx <= N
+#pragma unroll
+    for (int it = 0; it < EIT; ++it) {
+        const int e = threadIdx.x + it * NT;
+        if (e >= ROWS * nvec) break;
         const int r = e / nvec, i0 = (e % nvec) * V;
         const long long row = row0 + r;
         if (row >= nrows) continue;
