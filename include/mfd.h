@@ -70,8 +70,29 @@ typedef struct {
     long sample_every;
 } mfd_stepper;
 
-/* Execution: precision 32 (float) or 64 (double); device ordinal. */
-typedef struct { int precision_bits; int device; int reserved[6]; } mfd_exec;
+/* Execution: precision 32 (float) or 64 (double); device ordinal; z-slab
+ * decomposition over `world` ranks.
+ *   world = 1                    single GPU (the reference has no distribution)
+ *   world > 1, virtual_ranks = 1 all slabs on `device` (correctness harness)
+ *   world > 1, virtual_ranks = 0 one process per GPU, NCCL over NVLink; every rank
+ *                                passes the same nccl_id (mfd_nccl_unique_id on rank
+ *                                0, broadcast by the caller).  In this mode
+ *                                mfd_set_m_* / mfd_get_m_* move the rank's slab
+ *                                (planes [rank*nz/world, (rank+1)*nz/world)); all
+ *                                other calls are collective.
+ * nz must be divisible by world. */
+typedef struct {
+    int precision_bits;
+    int device;
+    int world;
+    int rank;
+    int virtual_ranks;
+    int reserved[3];
+    unsigned char nccl_id[128];
+} mfd_exec;
+
+/* NCCL unique id for a multi-GPU context (call on rank 0). */
+mfd_status mfd_nccl_unique_id(unsigned char id[128]);
 
 /* TrajectorySample (dynamics.hpp:138-144). */
 typedef struct {

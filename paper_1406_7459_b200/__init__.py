@@ -60,7 +60,8 @@ class _Stepper(C.Structure):
 
 
 class _Exec(C.Structure):
-    _fields_ = [("precision_bits", C.c_int), ("device", C.c_int), ("reserved", C.c_int * 6)]
+    _fields_ = [("precision_bits", C.c_int), ("device", C.c_int), ("world", C.c_int), ("rank", C.c_int),
+                ("virtual_ranks", C.c_int), ("reserved", C.c_int * 3), ("nccl_id", C.c_ubyte * 128)]
 
 
 class _Sample(C.Structure):
@@ -111,6 +112,7 @@ def load_library() -> C.CDLL:
         "mfd_stability_dt_limit": (C.c_double, [C.POINTER(_Material), C.POINTER(_Grid)]),
         "mfd_last_error": (C.c_char_p, [V]),
         "mfd_version": (C.c_char_p, []),
+        "mfd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "mfd_set_demag_octant_f64": (C.c_int, [V, _PD]),
         "mfd_get_demag_octant_f64": (C.c_int, [V, _PD]),
         "mfd_get_spectrum_octant_f64": (C.c_int, [V, _PD]),
@@ -212,10 +214,16 @@ class Simulation:
 
     def __init__(self, grid: Grid, material: Material, fields: FieldConfig = FieldConfig(),
                  stepper: StepperConfig = StepperConfig(), precision: int = 64, device: int = 0,
-                 init_direction: Sequence[float] = (0.0, 0.0, 1.0)):
+                 init_direction: Sequence[float] = (0.0, 0.0, 1.0), world: int = 1, rank: int = 0,
+                 virtual_ranks: bool = False, nccl_id: Optional[bytes] = None):
+        """world > 1: z-slab decomposition (mfd.h mfd_exec).  virtual_ranks runs
+        all slabs on `device`; otherwise one process per GPU over NCCL, with
+        set_m / get_m moving this rank's slab."""
         self.lib = load_library()
         self.grid, self.material, self.fields, self.stepper = grid, material, fields, stepper
         self.precision = precision
+        self.world, self.rank = world, rank
+        self.local = world > 1 and not virtual_ranks
         self._g = _Grid(grid.nx, grid.ny, grid.nz, grid.dx, grid.dy, grid.dz)
         self._m = _Material(material.A, material.Ku, material.Ms, material.alpha, material.gamma,
                             (C.c_double * 3)(*material.easy_axis))
@@ -223,14 +231,16 @@ class Simulation:
                          int(fields.zeeman), (C.c_double * 3)(*fields.extern_field))
         self._s = _Stepper(stepper.dt, stepper.renormalize_every, stepper.max_steps,
                            stepper.torque_tol_deg_per_ns, stepper.sample_every)
-        self._e = _Exec(precision, device)
+        self._e = _Exec(precision, device, world, rank, int(virtual_ranks))
+        if nccl_id is not None:
+            C.memmove(self._e.nccl_id, bytes(nccl_id), 128)
         h = C.c_void_p()
         rc = self.lib.mfd_create(C.byref(self._g), C.byref(self._m), C.byref(self._t),
                                  C.byref(self._s), C.byref(self._e), C.byref(h))
         if rc != 0:
             raise _ERR.get(rc, RuntimeError)(self.lib.mfd_last_error(None).decode())
         self.h = h
-        self.n = grid.cell_count
+        self.n = grid.cell_count // world if self.local else grid.cell_count
         d = np.asarray(init_direction, dtype=np.float64)
         self._check(self.lib.mfd_set_m_uniform(self.h, _ptr(d)))
 
@@ -391,6 +401,16 @@ class Simulation:
         m = _Material(material.A, material.Ku, material.Ms, material.alpha, material.gamma,
                       (C.c_double * 3)(*material.easy_axis))
         return lib.mfd_stability_dt_limit(C.byref(m), C.byref(g))
+
+
+def nccl_unique_id() -> bytes:
+    """NCCL unique id for a multi-GPU context (rank 0; broadcast it to the other ranks)."""
+    lib = load_library()
+    buf = (C.c_ubyte * 128)()
+    rc = lib.mfd_nccl_unique_id(buf)
+    if rc != 0:
+        raise OSError(lib.mfd_last_error(None).decode())
+    return bytes(buf)
 
 
 def padded_size(n: int) -> int:

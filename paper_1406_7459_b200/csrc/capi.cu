@@ -60,6 +60,10 @@ extern "C" {
 
 const char* mfd_version(void) { return "magfd-b200 0.1 (sm_100a)"; }
 
+mfd_status mfd_nccl_unique_id(unsigned char id[128]) {
+    return guard(nullptr, [&] { mfd::nccl_unique_id(id); });
+}
+
 mfd_status mfd_create(const mfd_grid* grid, const mfd_material* mat, const mfd_terms* terms,
                       const mfd_stepper* stepper, const mfd_exec* exec, mfd_ctx** out) {
     *out = nullptr;
@@ -76,10 +80,21 @@ mfd_status mfd_create(const mfd_grid* grid, const mfd_material* mat, const mfd_t
         mfd::ck(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
         if (p.major != 10) throw mfd::Error(MFD_ECUDA, "magfd-b200: built for sm_100a, device is sm_" +
                                                            std::to_string(p.major) + std::to_string(p.minor));
+        const int world = exec && exec->world > 1 ? exec->world : 1;
+        const int rank = exec ? exec->rank : 0;
+        if (world > 1 && grid->nz % world != 0)
+            throw mfd::Error(MFD_EINVAL, "magfd-b200: nz must be divisible by the number of GPUs (z-slab decomposition)");
+        if (world > 1 && (rank < 0 || rank >= world)) throw mfd::Error(MFD_EINVAL, "mfd_create: rank out of range");
         auto c = std::make_unique<mfd_ctx>();
         c->st = *stepper;
-        if (prec == 32) c->eng = std::make_unique<mfd::Engine<float>>(*grid, *mat, *terms, *stepper, dev);
-        else c->eng = std::make_unique<mfd::Engine<double>>(*grid, *mat, *terms, *stepper, dev);
+        if (world > 1 && exec->virtual_ranks) {
+            c->eng.reset(prec == 32 ? mfd::make_virtual_group<float>(*grid, *mat, *terms, *stepper, dev, world)
+                                    : mfd::make_virtual_group<double>(*grid, *mat, *terms, *stepper, dev, world));
+        } else {
+            mfd::Transport* tr = world > 1 ? mfd::make_nccl_transport(exec->nccl_id, rank, world, dev) : nullptr;
+            c->eng.reset(prec == 32 ? mfd::make_engine<float>(*grid, *mat, *terms, *stepper, dev, rank, world, tr)
+                                    : mfd::make_engine<double>(*grid, *mat, *terms, *stepper, dev, rank, world, tr));
+        }
         *out = c.release();
     });
 }

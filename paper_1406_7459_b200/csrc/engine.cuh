@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -58,6 +59,50 @@ void with_pow2(int L, F&& f) {
 
 template <class T> __global__ void k_ybuf(int Py, int Hy, int* out);
 
+// Collective transport of the z-slab decomposition.
+// One implementation per backend; the engine only calls these between its
+// passes, on its own stream (so they are captured into the step graphs).
+struct Transport {
+    virtual ~Transport() = default;
+    // all-to-all of `world` equal contiguous blocks: block p of send -> rank p,
+    // block q of recv <- rank q.
+    virtual void alltoall(const void* send, void* recv, size_t blk_bytes, cudaStream_t s) = 0;
+    // one-plane halo of the slab: planes 0 / nzl-1 of each component (stride
+    // comp_stride bytes, plane_bytes each) go to rank-1 / rank+1; the
+    // neighbours' planes land in lo / hi ([3][plane]).
+    virtual void halo(const void* m, size_t comp_stride, size_t plane_bytes, int nzl, void* lo, void* hi,
+                      cudaStream_t s) = 0;
+    virtual void allreduce_max_u64(unsigned long long* p, int n, cudaStream_t s) = 0;
+    virtual void allreduce_max_i32(int* p, int n, cudaStream_t s) = 0;
+    virtual void allreduce_sum_f64(double* p, int n, cudaStream_t s) = 0;
+    virtual void barrier(cudaStream_t s) = 0;
+};
+// NCCL transport over NVLink/NVSwitch (nccl_transport.cu).
+Transport* make_nccl_transport(const unsigned char id[128], int rank, int world, int device);
+void nccl_unique_id(unsigned char id[128]);
+
+class EngineBase;
+// Factories (defined per precision in engine_f32.cu / engine_f64.cu).
+template <class T>
+EngineBase* make_engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st,
+                        int device, int rank, int world, Transport* tr);
+template <class T>
+EngineBase* make_virtual_group(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
+                               const mfd_stepper& st, int device, int world);
+
+// Slab of a rank: planes [k0, k0+nzl) of the global nz, x-bin block rank.
+struct Slab {
+    int rank = 0, world = 1, k0 = 0, nzl = 0;
+    static Slab of(int nz, int rank, int world) {
+        Slab s;
+        s.rank = rank;
+        s.world = world;
+        s.nzl = nz / world;
+        s.k0 = rank * s.nzl;
+        return s;
+    }
+};
+
 // One iteration of the per-step pipeline as enqueued in a graph.
 struct Iter {
     int update = 1;
@@ -101,10 +146,17 @@ public:
     int precision = 64;
 };
 
+template <class T> class VirtualGroup;
+
 template <class T>
 class Engine final : public EngineBase {
+    friend class VirtualGroup<T>;
+
 public:
-    Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st, int device);
+    // slab / tr: z-slab of a multi-GPU run (tr = null with world > 1: the
+    // passes are orchestrated externally, e.g. by VirtualGroup).
+    Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st, int device,
+           Slab slab = Slab{}, Transport* tr = nullptr);
     ~Engine() override;
 
     void set_m(const double* x, const double* y, const double* z) override;
@@ -131,6 +183,15 @@ public:
 private:
     void build_tensor_from_octant();
     void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr);
+    // pass groups of one iteration: A = K1,K2 (slab -> send blocks), B = K3
+    // (receive blocks, full z), C = K4,K5 (send blocks -> slab + LLG)
+    void enq_A(const Iter& it, int cur, cudaEvent_t* ev = nullptr);
+    void enq_B(const Iter& it);
+    void enq_C(const Iter& it, int cur, cudaEvent_t* ev = nullptr);
+    void enq_local(const Iter& it, int cur);
+    Ctl make_ctl(const Iter& it) const;
+    StepIO make_io(const Iter& it) const;
+    Halo<T> halo_ptrs() const;
     void run_chunk(const std::vector<Iter>& its, int cur);
     void fetch_chunk(int n, std::vector<double>& torque, int& err);
     double torque_of(unsigned long long bits) const;
@@ -150,12 +211,16 @@ private:
     T scale_{};
     int Py_ = 2, Pz_ = 2, Hy_ = 2, Hz_ = 2;
 
+    Slab slab_;
+    Transport* tr_ = nullptr;           // owned
     cudaStream_t stream_ = nullptr;
     T* M_[2] = {nullptr, nullptr};
     int cur_ = 0;
     T* H_ = nullptr;                     // H_eff / H_demag output
+    T* halo_ = nullptr;                  // [2][3][ny][nx]: lo, hi planes (world > 1)
     C2<T>* A_ = nullptr;
-    C2<T>* B_ = nullptr;
+    C2<T>* B_ = nullptr;                 // send-side blocks (== receive side on one GPU)
+    C2<T>* Br_ = nullptr;                // receive-side blocks (world > 1)
     T* Kt_ = nullptr;
     C2<T>* tw_ = nullptr;
     int* ybuf_ = nullptr;

@@ -39,9 +39,12 @@ static void set_smem(const void* fn, int bytes) {
 
 template <class T>
 Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st,
-                  int device)
-    : grid_(g), mat_(m), terms_(te), st_(st), device_(device) {
+                  int device, Slab slab, Transport* tr)
+    : grid_(g), mat_(m), terms_(te), st_(st), device_(device), slab_(slab), tr_(tr) {
     precision = sizeof(T) == 4 ? 32 : 64;
+    if (slab_.world <= 1) slab_ = Slab::of(g.nz, 0, 1);
+    if (slab_.world > 1 && (g.nz % slab_.world != 0))
+        throw Error(MFD_EINVAL, "magfd-b200: nz must be divisible by the number of GPUs (z-slab decomposition)");
     ck(cudaSetDevice(device_), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
     const int Px = padded_size(g.nx);
@@ -49,12 +52,23 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     Pz_ = padded_size(g.nz);
     if (Px / 2 > kMaxL || Py_ > kMaxL || Pz_ > kMaxL)
         throw Error(MFD_EINVAL, "magfd-b200: padded FFT size exceeds the engine limit (nx <= 2048, ny,nz <= 1024)");
-    geo_.nx = g.nx; geo_.ny = g.ny; geo_.nz = g.nz;
+    const int G = slab_.world, nzl = slab_.nzl;
+    geo_.nx = g.nx; geo_.ny = g.ny; geo_.nz = nzl;
     geo_.Px = Px; geo_.Py = Py_; geo_.Pz = Pz_;
     geo_.N = Px / 2;
     geo_.Hx = geo_.N + 1;
     geo_.Hp = (geo_.Hx + 15) / 16 * 16;
-    geo_.ncell = (long long)g.nx * g.ny * g.nz;
+    geo_.ncell = (long long)g.nx * g.ny * nzl;
+    geo_.nzg = g.nz;
+    geo_.k0 = slab_.k0;
+    geo_.G = G;
+    geo_.ublk = slab_.rank;
+    // x-bin blocks: multiples of 16 so no y/z tile straddles two ranks
+    geo_.Wb = G == 1 ? geo_.Hp : ((geo_.Hx + G - 1) / G + 15) / 16 * 16;
+    geo_.Hv = std::max(0, std::min(geo_.Wb, geo_.Hx - slab_.rank * geo_.Wb));
+    geo_.S_k = (long long)Py_ * geo_.Wb;
+    geo_.S_c = (long long)nzl * geo_.S_k;
+    geo_.S_blk = 3 * geo_.S_c;
     ncell = geo_.ncell;
     Hy_ = Py_ / 2 + 1;
     Hz_ = Pz_ / 2 + 1;
@@ -103,11 +117,14 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     ck(cudaMallocHost((void**)&h_sums_, kMaxChunk * 8 * sizeof(double)), "host alloc");
     ck(cudaMallocHost((void**)&h_err_, sizeof(int)), "host alloc");
 
+    if (G > 1) alloc(&halo_, 2 * 3 * (long long)g.nx * g.ny * sizeof(T));
     if (terms_.demag) {
-        const long long nrows = (long long)g.ny * g.nz;
+        const long long nrows = (long long)g.ny * nzl;
         alloc(&A_, 3 * nrows * geo_.Hp * sizeof(C2<T>));
-        alloc(&B_, 3 * (long long)g.nz * Py_ * geo_.Hp * sizeof(C2<T>));
-        alloc(&Kt_, 6 * (long long)Hy_ * Hz_ * geo_.Hp * sizeof(T));
+        alloc(&B_, (size_t)G * geo_.S_blk * sizeof(C2<T>));
+        if (G > 1) alloc(&Br_, (size_t)G * geo_.S_blk * sizeof(C2<T>));
+        else Br_ = B_;
+        alloc(&Kt_, 6 * (long long)Hy_ * Hz_ * geo_.Wb * sizeof(T));
         alloc(&ybuf_, Py_ * sizeof(int));   // buffer row of every y frequency
         // twiddles exp(-2 pi i k / TWN), long double on the host, cast to T (fft.hpp:70-74)
         std::vector<C2<T>> tw(TWN);
@@ -136,8 +153,9 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             if constexpr (z_variant<T, L>() == 2) set_smem<T>((const void*)k_fft_z_conv2<T, L>, Z2Cfg<T, L>::SMEM);
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
-        // tensor octant on the device (K0a), then spectra (K0b)
-        alloc(&oct_, 6 * n * sizeof(double));
+        // tensor octant on the device (K0a, the whole global octant), then
+        // spectra (K0b) of this rank's x-bin block
+        alloc(&oct_, 6 * (long long)g.nx * g.ny * g.nz * sizeof(double));
         launch_tensor_octant(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, oct_, stream_);
         ck(cudaGetLastError(), "k_tensor_octant");
         build_tensor_from_octant();
@@ -152,9 +170,11 @@ template <class T>
 Engine<T>::~Engine() {
     cudaSetDevice(device_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, oct_, err_, torque_, sums_, partials_, ticket_};
+    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, oct_, err_, torque_, sums_, partials_, ticket_, halo_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (Br_ && Br_ != B_) cudaFree(Br_);
+    delete tr_;
     if (h_torque_) cudaFreeHost(h_torque_);
     if (h_sums_) cudaFreeHost(h_sums_);
     if (h_err_) cudaFreeHost(h_err_);
@@ -165,9 +185,9 @@ Engine<T>::~Engine() {
 // K0b: separable cosine/sine transforms of the fp64 octant -> real spectrum octant in T.
 template <class T>
 void Engine<T>::build_tensor_from_octant() {
-    const int nx = grid_.nx, ny = grid_.ny, nz = grid_.nz;
-    const int Hx = geo_.Hx, Hp = geo_.Hp;
-    const long long n = geo_.ncell;
+    const int nx = grid_.nx, ny = grid_.ny, nz = grid_.nz;   // global grid
+    const int Hx = geo_.Hx, Wb = geo_.Wb, u0 = geo_.ublk * geo_.Wb;
+    const long long n = (long long)nx * ny * nz;
     double *Cx[2], *Cy[2], *Cz[2], *T1, *T2;
     auto mat = [&](double** C, int H, int nn, int P) {
         for (int odd = 0; odd < 2; ++odd) {
@@ -195,13 +215,16 @@ void Engine<T>::build_tensor_from_octant() {
         d.a_m = ny; d.a_k = 1; d.b_k = Hx; d.b_n = 1; d.o_m = Hx; d.o_n = 1;
         d.b_b1 = (long long)ny * Hx; d.o_b1 = (long long)Hy_ * Hx; d.nb2 = 1; d.scale = 1.0;
         launch_gemm64(d, nz, Cy[oy[c]], T1, T2, stream_);
-        // z: Kt[v][w][u][c] = s * sum_k Cz[w][k] T2[k][v][u];  two odd axes give (-2i)^2 = -4 -> s = -1.
-        // The six components of a bin are interleaved so K3 reads them as three vectors.
-        d = GemmDesc{};
-        d.Mdim = Hz_; d.Ndim = Hx; d.Kdim = nz;
-        d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = 6LL * Hp; d.o_n = 6;
-        d.b_b1 = Hx; d.o_b1 = 6LL * Hz_ * Hp; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
-        launch_gemm64(d, Hy_, Cz[oz[c]], T2, Kt_ + c, stream_);
+        // z: Kt[v][w][u][c] = s * sum_k Cz[w][k] T2[k][v][u0+u] for this rank's x-bin block;
+        // two odd axes give (-2i)^2 = -4 -> s = -1.  The six components of a
+        // bin are interleaved so K3 reads them as three vectors.
+        if (geo_.Hv > 0) {
+            d = GemmDesc{};
+            d.Mdim = Hz_; d.Ndim = geo_.Hv; d.Kdim = nz;
+            d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = 6LL * Wb; d.o_n = 6;
+            d.b_b1 = Hx; d.o_b1 = 6LL * Hz_ * Wb; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
+            launch_gemm64(d, Hy_, Cz[oz[c]], T2 + u0, Kt_ + c, stream_);
+        }
         ck(cudaGetLastError(), "tensor gemm");
     }
     ck(cudaStreamSynchronize(stream_), "tensor setup");
@@ -217,20 +240,23 @@ void Engine<T>::build_tensor_from_octant() {
 template <class T>
 void Engine<T>::set_octant(const double* oct) {
     if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
-    ck(cudaMemcpy(oct_, oct, 6 * geo_.ncell * sizeof(double), cudaMemcpyHostToDevice), "octant upload");
+    ck(cudaMemcpy(oct_, oct, 6 * (long long)grid_.nx * grid_.ny * grid_.nz * sizeof(double), cudaMemcpyHostToDevice),
+       "octant upload");
     build_tensor_from_octant();
 }
 
 template <class T>
 void Engine<T>::get_octant(double* oct) {
     if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
-    ck(cudaMemcpy(oct, oct_, 6 * geo_.ncell * sizeof(double), cudaMemcpyDeviceToHost), "octant download");
+    ck(cudaMemcpy(oct, oct_, 6 * (long long)grid_.nx * grid_.ny * grid_.nz * sizeof(double), cudaMemcpyDeviceToHost),
+       "octant download");
 }
 
 template <class T>
 void Engine<T>::get_spectrum(double* out) {
     if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
-    const long long cnt = 6LL * Hy_ * Hz_ * geo_.Hp;
+    if (geo_.G != 1) throw Error(MFD_EINVAL, "get_spectrum: single-GPU contexts only");
+    const long long cnt = 6LL * Hy_ * Hz_ * geo_.Wb;
     std::vector<T> h(cnt);
     ck(cudaMemcpy(h.data(), Kt_, cnt * sizeof(T), cudaMemcpyDeviceToHost), "spectrum download");
     const int Hx = geo_.Hx;
@@ -239,16 +265,18 @@ void Engine<T>::get_spectrum(double* out) {
             for (int w = 0; w < Hz_; ++w)
                 for (int u = 0; u < Hx; ++u)
                     out[(((long long)c * Hy_ + v) * Hz_ + w) * Hx + u] =
-                        (double)h[(((long long)v * Hz_ + w) * geo_.Hp + u) * 6 + c];
+                        (double)h[(((long long)v * Hz_ + w) * geo_.Wb + u) * 6 + c];
 }
 
 // --------------------------------------------------------------- enqueue
 template <class T>
-void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
-    const T* Mc = M_[cur];
-    T* Mn = M_[cur ^ 1];
-    Ctl ctl{err_, it.check_prev && it.slot > 0 ? torque_ + it.slot - 1 : nullptr, mat_.Ms,
-            st_.torque_tol_deg_per_ns, kRadToDegPerNs};
+Ctl Engine<T>::make_ctl(const Iter& it) const {
+    return Ctl{err_, it.check_prev && it.slot > 0 ? torque_ + it.slot - 1 : nullptr, mat_.Ms,
+               st_.torque_tol_deg_per_ns, kRadToDegPerNs};
+}
+
+template <class T>
+StepIO Engine<T>::make_io(const Iter& it) const {
     StepIO io{};
     io.update = it.update;
     io.renorm = it.renorm;
@@ -259,62 +287,127 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
     io.partials = partials_;
     io.sums_out = sums_ + 8 * it.slot;
     io.ticket = ticket_;
-    if (events) ck(cudaEventRecord(ev[0], stream_), "event");
-    if (!terms_.demag) {
-        k_local_llg<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(geo_, Mc, Mn, H_, lp_, io, ctl);
-        if (events)
-            for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
-        return;
-    }
+    return io;
+}
+
+template <class T>
+Halo<T> Engine<T>::halo_ptrs() const {
+    const long long plane = 3LL * grid_.nx * grid_.ny;
+    Halo<T> h{nullptr, nullptr};
+    if (slab_.world > 1 && slab_.rank > 0) h.lo = halo_;
+    if (slab_.world > 1 && slab_.rank < slab_.world - 1) h.hi = halo_ + plane;
+    return h;
+}
+
+template <class T>
+void Engine<T>::enq_local(const Iter& it, int cur) {
+    k_local_llg<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
+        geo_, M_[cur], M_[cur ^ 1], H_, lp_, make_io(it), make_ctl(it), halo_ptrs());
+}
+
+// A: K1 (x, R2C) + K2 (y forward) -> send blocks B_
+template <class T>
+void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev) {
+    const Ctl ctl = make_ctl(it);
     const long long nrows = (long long)geo_.ny * geo_.nz;
     with_pow2(geo_.N, [&]<int L>() {
         using CF = XCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
-        k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Mc, A_, tw_, ctl);
+        k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
     });
-    if (events) ck(cudaEventRecord(ev[1], stream_), "event");
+    if (ev) ck(cudaEventRecord(ev[1], stream_), "event");
     if (stop_after_ == 1) return;
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         k_fft_y_fwd<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
     });
-    if (events) ck(cudaEventRecord(ev[2], stream_), "event");
-    if (stop_after_ == 2) return;
+}
+
+// B: K3 on the receive blocks Br_ (this rank's x-bin block, all z)
+template <class T>
+void Engine<T>::enq_B(const Iter& it) {
+    const Ctl ctl = make_ctl(it);
+    if (geo_.Hv <= 0) return;
     with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
-            dim3 grid((geo_.Hx + 31) / 32, Hy_, 1);
-            k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, B_, Kt_, ybuf_, ctl);
+            dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
+            k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, Br_, Kt_, ybuf_, ctl);
         } else if constexpr (z_variant<T, L>() == 2) {
             using CF = Z2Cfg<T, L>;
-            dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
-            k_fft_z_conv2<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
+            k_fft_z_conv2<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
         } else {
             using CF = ZCfg<T, L>;
-            dim3 grid((geo_.Hx + CF::W - 1) / CF::W, Hy_, 1);
-            k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
+            k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
         }
     });
-    if (events) ck(cudaEventRecord(ev[3], stream_), "event");
-    if (stop_after_ == 3) return;
+}
+
+// C: K4 (y inverse, send blocks -> A) + K5 (x inverse + H_eff + LLG + Euler)
+template <class T>
+void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
+    const Ctl ctl = make_ctl(it);
+    const StepIO io = make_io(it);
+    const Halo<T> hl = halo_ptrs();
+    const long long nrows = (long long)geo_.ny * geo_.nz;
+    const T* Mc = M_[cur];
+    T* Mn = M_[cur ^ 1];
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         k_fft_y_inv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
     });
-    if (events) ck(cudaEventRecord(ev[4], stream_), "event");
+    if (ev) ck(cudaEventRecord(ev[4], stream_), "event");
     if (stop_after_ == 4) return;
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
         if (geo_.nx % V16<T>::V == 0 && io.sums)
-            k_c2r_x_llg_v<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+            k_c2r_x_llg_v<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io,
+                                                                            ctl, hl);
         else if (geo_.nx % V16<T>::V == 0)
-            k_c2r_x_llg_v<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+            k_c2r_x_llg_v<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_,
+                                                                             io, ctl, hl);
         else
-            k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl);
+            k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl,
+                                                                    hl);
     });
-    if (events) ck(cudaEventRecord(ev[5], stream_), "event");
+}
+
+// One iteration.  Multi-GPU (tr_ set): M halo, the two all-to-all transposes
+// around K3 and the scalar allreduces are issued on the same stream, so they
+// are captured into the step graph with the kernels.
+template <class T>
+void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
+    const size_t tsz = sizeof(T);
+    if (events) ck(cudaEventRecord(ev[0], stream_), "event");
+    if (tr_ && slab_.world > 1)
+        tr_->halo(M_[cur], geo_.ncell * tsz, (size_t)grid_.nx * grid_.ny * tsz, geo_.nz, halo_,
+                  halo_ + 3LL * grid_.nx * grid_.ny, stream_);
+    if (!terms_.demag) {
+        enq_local(it, cur);
+        if (events)
+            for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
+    } else {
+        enq_A(it, cur, events ? ev : nullptr);
+        if (events) ck(cudaEventRecord(ev[2], stream_), "event");
+        if (stop_after_ == 1 || stop_after_ == 2) return;
+        if (tr_ && slab_.world > 1) tr_->alltoall(B_, Br_, geo_.S_blk * sizeof(C2<T>), stream_);
+        enq_B(it);
+        if (events) ck(cudaEventRecord(ev[3], stream_), "event");
+        if (stop_after_ == 3) return;
+        if (tr_ && slab_.world > 1) tr_->alltoall(Br_, B_, geo_.S_blk * sizeof(C2<T>), stream_);
+        enq_C(it, cur, events ? ev : nullptr);
+        if (events) ck(cudaEventRecord(ev[5], stream_), "event");
+        if (stop_after_ == 4) return;
+    }
+    if (tr_ && slab_.world > 1) {
+        tr_->allreduce_max_u64(torque_ + it.slot, 1, stream_);
+        tr_->allreduce_max_i32(err_, 1, stream_);
+        if (it.sums) tr_->allreduce_sum_f64(sums_ + 8 * it.slot, 7, stream_);
+    }
 }
 
 // Launch a chunk of iterations (one CUDA graph, cached by its shape).
@@ -559,7 +652,7 @@ mfd_sample Engine<T>::make_sample(const double s[8], double torque) const {
     mfd_sample o{};
     o.step = stepno;
     o.t = t;
-    const double sc = 1.0 / (mat_.Ms * (double)geo_.ncell);
+    const double sc = 1.0 / (mat_.Ms * ((double)grid_.nx * grid_.ny * grid_.nz));   // global N
     o.m[0] = s[0] * sc;
     o.m[1] = s[1] * sc;
     o.m[2] = s[2] * sc;

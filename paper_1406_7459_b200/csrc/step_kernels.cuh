@@ -53,14 +53,33 @@ template <class T, int L> struct ZCfg {   // K3
     static constexpr int SMEM = NCOL * L * CS;
 };
 
+// Geometry of one rank's share of the problem.  Single GPU: G = 1, the slab
+// is the whole grid and the spectral layout is [1][3][nz][Py][Hp].
+// z-slab decomposition over G ranks: the rank owns
+// planes [k0, k0+nz) of nzg for the x/y passes and the LLG update, and x-bin
+// block `ublk` (width Wb, Hv valid) of every z column for the z pass.  The
+// y-spectrum B is laid out [block][3][nz][Py][Wb]: block b of the send side
+// goes to rank b, block g of the receive side came from rank g, so the two
+// all-to-all transposes move contiguous blocks and no pack kernel exists.
 struct Geo {
-    int nx, ny, nz;
-    int Px, Py, Pz;
-    int N;     // Px/2 complex points per x row
-    int Hx;    // N + 1 bins
-    int Hp;    // padded pitch of A/B/Kt rows
-    long long ncell;
+    int nx, ny, nz;       // nz: planes of this rank's slab
+    int Px, Py, Pz;       // Pz from the global nzg
+    int N;                // Px/2 complex points per x row
+    int Hx;               // N + 1 bins
+    int Hp;               // pitch of A rows
+    long long ncell;      // cells of the slab
+    int nzg, k0;          // global planes, first plane of the slab
+    int G, ublk, Wb, Hv;  // ranks, this rank's x-bin block, block width, valid bins in it
+    long long S_blk, S_c, S_k;   // B strides: block, component, plane (row stride Wb)
 };
+// z offset of global plane k in the receive-side layout (rank k / nz, plane k % nz).
+__device__ __forceinline__ long long zoff(const Geo& g, int k) {
+    if (g.G == 1) return (long long)k * g.S_k;
+    return (long long)(k / g.nz) * g.S_blk + (long long)(k % g.nz) * g.S_k;
+}
+// One-plane M halos below / above the slab ([3][ny][nx] each; null at the
+// global boundary or on a single GPU).
+template <class T> struct Halo { const T* lo; const T* hi; };
 
 // Step control: early exit after a non-finite update (error) or, in relax
 // mode, once the previous iteration met the torque criterion
@@ -150,8 +169,9 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
     const int u0 = blockIdx.x * W;
     const int k = blockIdx.y, comp = blockIdx.z;
     const C2<T>* src = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
-    C2<T>* dst = B + ((long long)comp * g.nz + k) * L * g.Hp + u0;
-    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx;
+    // tiles never straddle a block: Wb is a multiple of 16 >= W
+    C2<T>* dst = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
+    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx, Wb = g.Wb;
     auto ld0 = [&](int col, int pos) -> C2<T> {
         if (pos >= ny || u0 + col >= Hx) return mk<T>(0, 0);
         return src[(long long)pos * Hp + col];
@@ -159,7 +179,7 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
     auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
     auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
     auto stn = [&](int col, int pos, C2<T> v) {
-        if (u0 + col < Hx) dst[(long long)pos * Hp + col] = v;
+        if (u0 + col < Hx) dst[(long long)pos * Wb + col] = v;
     };
     fft_forward<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
 }
@@ -175,12 +195,12 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
     const int k = blockIdx.y, comp = blockIdx.z;
-    const C2<T>* src = B + ((long long)comp * g.nz + k) * L * g.Hp + u0;
+    const C2<T>* src = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
     C2<T>* dst = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
-    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx;
+    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx, Wb = g.Wb;
     auto ld0 = [&](int col, int pos) -> C2<T> {
         if (u0 + col >= Hx) return mk<T>(0, 0);
-        return src[(long long)pos * Hp + col];
+        return src[(long long)pos * Wb + col];
     };
     auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
     auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
@@ -204,20 +224,18 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
-    const int u0 = blockIdx.x * W;
+    const int u0 = blockIdx.x * W;               // x-bin within this rank's block
     const int v = blockIdx.y;                    // 0..Py/2
-    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int Py = g.Py, nz = g.nzg, Wb = g.Wb, Hv = g.Hv;
     const int vp = (Py - v) & (Py - 1);
     const bool pair = vp != v;
     const long long rowA = ybuf[v], rowB = ybuf[vp];   // buffer rows of v and Py-v
-    const long long cstride = (long long)nz * Py * Hp; // component stride in B
-    const long long kstride = (long long)Py * Hp;      // z-plane stride in B
     // column c = comp*2W + r*W + w  (r: 0 -> v, 1 -> Py-v)
     auto gaddr = [&](int col, int pos) -> long long {
         const int comp = col / (2 * W), r = (col / W) & 1, w = col % W;
-        return comp * cstride + (long long)pos * kstride + (r ? rowB : rowA) * Hp + u0 + w;
+        return comp * g.S_c + zoff(g, pos) + (r ? rowB : rowA) * Wb + u0 + w;
     };
-    auto valid = [&](int col) { return u0 + (col % W) < Hx && (pair || ((col / W) & 1) == 0); };
+    auto valid = [&](int col) { return u0 + (col % W) < Hv && (pair || ((col / W) & 1) == 0); };
     auto ld0 = [&](int col, int pos) -> C2<T> {
         if (pos >= nz || !valid(col)) return mk<T>(0, 0);
         return B[gaddr(col, pos)];
@@ -231,11 +249,11 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
     __syncthreads();
     // K~ . M~ : thread task (w, wq) covers z-frequencies {wq, Pz-wq} and both y rows.
     const int Hz = L / 2 + 1;
-    const T* kbase = Kt + (((long long)v * Hz) * Hp + u0) * 6;
+    const T* kbase = Kt + (((long long)v * Hz) * Wb + u0) * 6;
     for (int e = threadIdx.x; e < W * Hz; e += NT) {
         const int w = e % W, wq = e / W;
-        if (u0 + w >= Hx) continue;
-        const T* kp = kbase + ((long long)wq * Hp + w) * 6;
+        if (u0 + w >= Hv) continue;
+        const T* kp = kbase + ((long long)wq * Wb + w) * 6;
         const T kxx = __ldg(kp), kyy = __ldg(kp + 1), kzz = __ldg(kp + 2);
         const T kxy = __ldg(kp + 3), kxz = __ldg(kp + 4), kyz = __ldg(kp + 5);
         const int wpart = (L - wq) & (L - 1);
@@ -305,16 +323,15 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
-    const int u0 = blockIdx.x * W;
+    const int u0 = blockIdx.x * W;               // x-bin within this rank's block
     const int v = blockIdx.y;
-    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int Py = g.Py, nz = g.nzg, Wb = g.Wb;
     const int vp = (Py - v) & (Py - 1);
     const bool pair = vp != v;
     const int w = threadIdx.x % W, n2 = (threadIdx.x / W) % R1, r = threadIdx.x / (W * R1);
-    const bool live = u0 + w < Hx && (pair || r == 0);
-    const long long cstride = (long long)nz * Py * Hp;
-    const long long kstride = (long long)Py * Hp;
-    C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Hp + u0 + w;   // + comp*cstride + k*kstride
+    const bool live = u0 + w < g.Hv && (pair || r == 0);
+    const long long cstride = g.S_c;
+    C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + zoff(k)
     // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + r * W + w;
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
@@ -327,7 +344,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int j = 0; j < R0 / 2; ++j) {
             const int pos = R1 * j + n2;
-            nxt[j] = (live && pos < nz) ? gcol[c * cstride + pos * kstride] : mk<T>(0, 0);
+            nxt[j] = (live && pos < nz) ? gcol[c * cstride + zoff(g, pos)] : mk<T>(0, 0);
         }
     };
     fetch(0);
@@ -362,12 +379,12 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int c = 0; c < 3; ++c) dft<T, R1, false>(y[c]);
         if (live) {
-            const T* kb = Kt + ((long long)v * Hz * Hp + u0 + w) * 6;
+            const T* kb = Kt + ((long long)v * Hz * Wb + u0 + w) * 6;
 #pragma unroll
             for (int k1 = 0; k1 < R1; ++k1) {
                 const int f = k0 + R0 * k1;
                 const bool hi = 2 * f > L;
-                kmul<T>(y[0][k1], y[1][k1], y[2][k1], kb + (long long)(hi ? L - f : f) * Hp * 6, sy,
+                kmul<T>(y[0][k1], y[1][k1], y[2][k1], kb + (long long)(hi ? L - f : f) * Wb * 6, sy,
                         hi ? T(-1) : T(1));
             }
         }
@@ -395,7 +412,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
             for (int j = 0; 2 * j < R0; ++j) {
                 const int pos = R1 * j + n2;
-                if (pos < nz) gcol[c * cstride + pos * kstride] = x[j];
+                if (pos < nz) gcol[c * cstride + zoff(g, pos)] = x[j];
             }
         }
     }
@@ -417,28 +434,28 @@ __global__ void __launch_bounds__(64)
 k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int* __restrict__ ybuf, Ctl ctl) {
     if (halted(ctl)) return;
     const int w = threadIdx.x & 31, r = threadIdx.x >> 5;
-    const int u = blockIdx.x * 32 + w;
+    const int u = blockIdx.x * 32 + w;           // x-bin within this rank's block
     const int v = blockIdx.y;
-    const int Py = g.Py, nz = g.nz, Hp = g.Hp, Hx = g.Hx;
+    const int Py = g.Py, nz = g.nzg, Wb = g.Wb;
     const int vp = (Py - v) & (Py - 1);
-    if (u >= Hx || (r == 1 && vp == v)) return;
+    if (u >= g.Hv || (r == 1 && vp == v)) return;
     const long long row = r ? ybuf[vp] : ybuf[v];
-    const long long cstride = (long long)nz * Py * Hp, kstride = (long long)Py * Hp;
-    C2<T>* base = B + row * Hp + u;
+    const long long cstride = g.S_c;
+    C2<T>* base = B + row * Wb + u;
     C2<T> x[3][L];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int k = 0; k < L; ++k) x[c][k] = (k < nz && 2 * k < L) ? base[c * cstride + k * kstride] : mk<T>(0, 0);
+        for (int k = 0; k < L; ++k) x[c][k] = (k < nz && 2 * k < L) ? base[c * cstride + zoff(g, k)] : mk<T>(0, 0);
 #pragma unroll
     for (int c = 0; c < 3; ++c) dft<T, L, false, true>(x[c]);
     const int Hz = L / 2 + 1;
-    const T* kb = Kt + ((long long)v * Hz * Hp + u) * 6;
+    const T* kb = Kt + ((long long)v * Hz * Wb + u) * 6;
     const T sy = r ? T(-1) : T(1);
 #pragma unroll
     for (int f = 0; f < L; ++f) {
         const bool hi = 2 * f > L;
-        kmul<T>(x[0][f], x[1][f], x[2][f], kb + (long long)(hi ? L - f : f) * Hp * 6, sy, hi ? T(-1) : T(1));
+        kmul<T>(x[0][f], x[1][f], x[2][f], kb + (long long)(hi ? L - f : f) * Wb * 6, sy, hi ? T(-1) : T(1));
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) dft<T, L, true, false, true>(x[c]);
@@ -446,7 +463,7 @@ k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int*
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int k = 0; k < L; ++k)
-            if (k < nz && 2 * k < L) base[c * cstride + k * kstride] = x[c][k];
+            if (k < nz && 2 * k < L) base[c * cstride + zoff(g, k)] = x[c][k];
 }
 
 // ------------------------------------------------------------------ K5
@@ -480,8 +497,8 @@ struct StepIO {
 template <class T>
 __device__ __forceinline__ void cell_update(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                             const T* __restrict__ M, T* __restrict__ Mn,
-                                            T* __restrict__ Hout, long long c, int i, int j, int k,
-                                            T hdx, T hdy, T hdz, double& tmax, double* acc,
+                                            T* __restrict__ Hout, const Halo<T>& hl, long long c, int i, int j,
+                                            int k, T hdx, T hdy, T hdz, double& tmax, double* acc,
                                             int& bad) {
     const long long n = g.ncell;
     const T mx = M[c], my = M[c + n], mz = M[c + 2 * n];
@@ -490,21 +507,27 @@ __device__ __forceinline__ void cell_update(const Geo& g, const LocalParams<T>& 
     if (P.exch) {
         T h0 = 0, h1 = 0, h2 = 0;
         const long long sy = g.nx, sz = (long long)g.nx * g.ny;
-        auto add = [&](long long nb, T w) {
-            h0 = add_rn(h0, mul_rn(w, sub_rn(M[nb], mx)));
-            h1 = add_rn(h1, mul_rn(w, sub_rn(M[nb + n], my)));
-            h2 = add_rn(h2, mul_rn(w, sub_rn(M[nb + 2 * n], mz)));
+        // neighbour values at q[0], q[cs], q[2cs] (cs = component stride)
+        auto add = [&](const T* q, long long cs, T w) {
+            h0 = add_rn(h0, mul_rn(w, sub_rn(q[0], mx)));
+            h1 = add_rn(h1, mul_rn(w, sub_rn(q[cs], my)));
+            h2 = add_rn(h2, mul_rn(w, sub_rn(q[2 * cs], mz)));
         };
-        auto link = [&](long long nb, double w) {
-            const double e0 = (double)M[nb] - mx, e1 = (double)M[nb + n] - my, e2 = (double)M[nb + 2 * n] - mz;
+        auto link = [&](const T* q, long long cs, double w) {
+            const double e0 = (double)q[0] - mx, e1 = (double)q[cs] - my, e2 = (double)q[2 * cs] - mz;
             elink += w * (e0 * e0 + e1 * e1 + e2 * e2);
         };
-        if (i > 0) add(c - 1, P.cx);
-        if (i < g.nx - 1) { add(c + 1, P.cx); if (io.sums) link(c + 1, P.wx); }
-        if (j > 0) add(c - sy, P.cy);
-        if (j < g.ny - 1) { add(c + sy, P.cy); if (io.sums) link(c + sy, P.wy); }
-        if (k > 0) add(c - sz, P.cz);
-        if (k < g.nz - 1) { add(c + sz, P.cz); if (io.sums) link(c + sz, P.wz); }
+        const int kg = g.k0 + k;
+        const long long inplane = c - (long long)k * sz;
+        const T* zlo = k > 0 ? M + c - sz : hl.lo + inplane;
+        const T* zhi = k < g.nz - 1 ? M + c + sz : hl.hi + inplane;
+        const long long zlo_cs = k > 0 ? n : sz, zhi_cs = k < g.nz - 1 ? n : sz;
+        if (i > 0) add(M + c - 1, n, P.cx);
+        if (i < g.nx - 1) { add(M + c + 1, n, P.cx); if (io.sums) link(M + c + 1, n, P.wx); }
+        if (j > 0) add(M + c - sy, n, P.cy);
+        if (j < g.ny - 1) { add(M + c + sy, n, P.cy); if (io.sums) link(M + c + sy, n, P.wy); }
+        if (kg > 0) add(zlo, zlo_cs, P.cz);
+        if (kg < g.nzg - 1) { add(zhi, zhi_cs, P.cz); if (io.sums) link(zhi, zhi_cs, P.wz); }
         Hx = add_rn(Hx, h0);
         Hy = add_rn(Hy, h1);
         Hz = add_rn(Hz, h2);
@@ -636,7 +659,7 @@ template <class T, int N>
 __global__ void __launch_bounds__(LCfg<T, N>::NT)
 k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
             T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io,
-            Ctl ctl) {
+            Ctl ctl, Halo<T> hl) {
     using CF = LCfg<T, N>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
     if (halted(ctl)) return;
@@ -694,7 +717,7 @@ k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __re
         const T hdx = (odd ? zx.y : zx.x) * scale;
         const T hdy = (odd ? zy.y : zy.x) * scale;
         const T hdz = (odd ? zz.y : zz.x) * scale;
-        cell_update<T>(g, P, io, M, Mn, Hout, row * nx + i, i, j, k, hdx, hdy, hdz, tmax, acc, bad);
+        cell_update<T>(g, P, io, M, Mn, Hout, hl, row * nx + i, i, j, k, hdx, hdy, hdz, tmax, acc, bad);
     }
     block_finish<NT>(io, ctl, tmax, acc, bad);
 }
@@ -825,12 +848,14 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 template <class T, bool SUMS>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                           const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
-                                          long long c0, int i0, int j, int k, const T (&hd)[3][V16<T>::V],
-                                          double& tmax, double* acc, int& bad) {
+                                          const Halo<T>& hl, long long c0, int i0, int j, int k,
+                                          const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad) {
     constexpr int V = V16<T>::V;
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
-    const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = k > 0, hz1 = k < g.nz - 1;
+    const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
+    const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = kg > 0, hz1 = kg < g.nzg - 1;
     const bool hx0 = i0 > 0, hx1 = i0 + V < g.nx;
+    const long long inplane = c0 - (long long)k * sz;  // j*nx + i0
     T m[3][V], H[3][V];
     double elink[V];
 #pragma unroll
@@ -847,8 +872,8 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         T ym[V], yp[V], zm[V], zp[V];
         if (hy0) vload<T>(p - sy, ym);
         if (hy1) vload<T>(p + sy, yp);
-        if (hz0) vload<T>(p - sz, zm);
-        if (hz1) vload<T>(p + sz, zp);
+        if (hz0) vload<T>(k > 0 ? p - sz : hl.lo + c * sz + inplane, zm);          // slab edge: halo plane
+        if (hz1) vload<T>(k < g.nz - 1 ? p + sz : hl.hi + c * sz + inplane, zp);
         const T xl = hx0 ? __ldg(p - 1) : T(0);
         const T xr = hx1 ? __ldg(p + V) : T(0);
 #pragma unroll
@@ -943,7 +968,8 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 template <class T, int N, bool SUMS>
 __global__ void __launch_bounds__(LCfg<T, N>::NT)
 k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
-              T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl) {
+              T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
+              Halo<T> hl) {
     using CF = LCfg<T, N>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
     constexpr int V = V16<T>::V;
@@ -1025,7 +1051,7 @@ k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __
                 hd[c][q] = z.x * scale;
                 hd[c][q + 1] = z.y * scale;
             }
-        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, row * nx + i0, i0, j, k, hd, tmax, acc, bad);
+        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad);
     }
     block_finish<NT>(io, ctl, tmax, acc, bad);
 }
@@ -1034,7 +1060,7 @@ k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __
 template <class T>
 __global__ void __launch_bounds__(256)
 k_local_llg(Geo g, const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout, LocalParams<T> P,
-            StepIO io, Ctl ctl) {
+            StepIO io, Ctl ctl, Halo<T> hl) {
     if (halted(ctl)) return;
     double tmax = 0;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -1044,7 +1070,7 @@ k_local_llg(Geo g, const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ 
         const int i = (int)(c % g.nx);
         const int j = (int)((c / g.nx) % g.ny);
         const int k = (int)(c / ((long long)g.nx * g.ny));
-        cell_update<T>(g, P, io, M, Mn, Hout, c, i, j, k, T(0), T(0), T(0), tmax, acc, bad);
+        cell_update<T>(g, P, io, M, Mn, Hout, hl, c, i, j, k, T(0), T(0), T(0), tmax, acc, bad);
     }
     block_finish<256>(io, ctl, tmax, acc, bad);
 }
