@@ -146,11 +146,16 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
         });
         with_pow2(Py_, [&]<int L>() {
-            set_smem<T>((const void*)k_fft_y_fwd<T, L>, YCfg<T, L>::SMEM);
-            set_smem<T>((const void*)k_fft_y_inv<T, L>, YCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_fft_y_fwd<T, L, true>, YCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_fft_y_inv<T, L, true>, YCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_fft_y_fwd<T, L, false>, YCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_fft_y_inv<T, L, false>, YCfg<T, L>::SMEM);
         });
         with_pow2(Pz_, [&]<int L>() {
-            if constexpr (z_variant<T, L>() == 2) set_smem<T>((const void*)k_fft_z_conv2<T, L>, Z2Cfg<T, L>::SMEM);
+            if constexpr (z_variant<T, L>() == 2) {
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, true>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, false>, Z2Cfg<T, L>::SMEM);
+            }
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
         // tensor octant on the device (K0a, the whole global octant), then
@@ -320,7 +325,10 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev) {
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
-        k_fft_y_fwd<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
+        if (2 * geo_.ny == L)
+            k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
+        else
+            k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
     });
 }
 
@@ -336,7 +344,10 @@ void Engine<T>::enq_B(const Iter& it) {
         } else if constexpr (z_variant<T, L>() == 2) {
             using CF = Z2Cfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
-            k_fft_z_conv2<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
+            if (2 * geo_.nzg == L)
+                k_fft_z_conv2<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
+            else
+                k_fft_z_conv2<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
         } else {
             using CF = ZCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
@@ -357,7 +368,10 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
-        k_fft_y_inv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
+        if (2 * geo_.ny == L)
+            k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
+        else
+            k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
     });
     if (ev) ck(cudaEventRecord(ev[4], stream_), "event");
     if (stop_after_ == 4) return;

@@ -30,7 +30,7 @@ template <class T, int L> constexpr int xpitch() { return L + (L >> padShift<T>(
 // -------------------------------------------------------------- configs
 template <class T, int N> struct XCfg {   // K1
     static constexpr int E = regE<T>();
-    static constexpr int ROWS = cmax(1, cmin(64, 256 * E / N));
+    static constexpr int ROWS = cmax(1, cmin(64, 128 * E / N));   // small CTAs: many independent phase schedules per SM
     static constexpr int NT = clampNT(cmax(128, ROWS * N / E));
     static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
 };
@@ -157,8 +157,26 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
     }
 }
 
+// Measured on B200 (512x512x64 f32): the swizzle removes the conflicts but the
+// extra integer work made K2 slower (0.32 -> 0.40 ms), so it is off.
+constexpr bool kYSwizzle = false;
+// y-pass shared tile [pos][W]: with 64-byte position rows, the last stage's
+// tasks (stride R_last positions apart) would land two per bank group; XOR the
+// row parity with the stride bit so a half-warp covers both 64-byte halves.
+template <class T, int L, int W>
+__device__ __forceinline__ int yswz(int pos) {
+    constexpr int S = Plan<T, L>::S;
+    constexpr int RL = S == 3 ? Plan<T, L>::R2 : S == 2 ? Plan<T, L>::R1 : 1;
+    if constexpr (kYSwizzle && W * (int)sizeof(C2<T>) == 64 && S >= 2) return pos ^ ((pos / RL) & 1);
+    else return pos;
+}
+
 // ------------------------------------------------------------------ K2
-template <class T, int L>
+// Tiles of W x-bins never leave the padded pitch (Hp and Wb are multiples of
+// 16 >= W), so x-bins >= Hx are computed as harmless padding columns instead
+// of being masked per element.  FY: ny == Py/2 (power-of-two ny), so the
+// pruned first stage never meets a row >= ny and the row test disappears.
+template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YCfg<T, L>::NT)
 k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
@@ -171,21 +189,19 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
     const C2<T>* src = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
     // tiles never straddle a block: Wb is a multiple of 16 >= W
     C2<T>* dst = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
-    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx, Wb = g.Wb;
+    const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
     auto ld0 = [&](int col, int pos) -> C2<T> {
-        if (pos >= ny || u0 + col >= Hx) return mk<T>(0, 0);
-        return src[(long long)pos * Hp + col];
+        if (!FY && pos >= ny) return mk<T>(0, 0);
+        return src[pos * Hp + col];
     };
-    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
-    auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
-    auto stn = [&](int col, int pos, C2<T> v) {
-        if (u0 + col < Hx) dst[(long long)pos * Wb + col] = v;
-    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[yswz<T, L, W>(pos) * W + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[yswz<T, L, W>(pos) * W + col] = v; };
+    auto stn = [&](int col, int pos, C2<T> v) { dst[pos * Wb + col] = v; };
     fft_forward<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
 }
 
 // ------------------------------------------------------------------ K4
-template <class T, int L>
+template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YCfg<T, L>::NT)
 k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
@@ -197,15 +213,12 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
     const int k = blockIdx.y, comp = blockIdx.z;
     const C2<T>* src = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
     C2<T>* dst = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
-    const int ny = g.ny, Hp = g.Hp, Hx = g.Hx, Wb = g.Wb;
-    auto ld0 = [&](int col, int pos) -> C2<T> {
-        if (u0 + col >= Hx) return mk<T>(0, 0);
-        return src[(long long)pos * Wb + col];
-    };
-    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * W + col]; };
-    auto sts = [&](int col, int pos, C2<T> v) { sm[pos * W + col] = v; };
+    const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
+    auto ld0 = [&](int col, int pos) -> C2<T> { return src[pos * Wb + col]; };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[yswz<T, L, W>(pos) * W + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[yswz<T, L, W>(pos) * W + col] = v; };
     auto stn = [&](int col, int pos, C2<T> v) {
-        if (pos < ny && u0 + col < Hx) dst[(long long)pos * Hp + col] = v;
+        if (FY || pos < ny) dst[pos * Hp + col] = v;   // pruned last stage: pos < Py/2 == ny when FY
     };
     fft_inverse<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
 }
@@ -313,7 +326,9 @@ template <class T, int L> struct Z2Cfg {
     static constexpr int SMEM = NCOL * L * CS;
 };
 
-template <class T, int L>
+// FZ: nz == Pz/2, so the pruned first/last stages never meet a plane >= nz.
+// Padding x-bins (>= Hv, inside the block pitch) are computed, not masked.
+template <class T, int L, bool FZ>
 __global__ void __launch_bounds__(Z2Cfg<T, L>::NT)
 k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
               const int* __restrict__ ybuf, Ctl ctl) {
@@ -329,7 +344,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     const int vp = (Py - v) & (Py - 1);
     const bool pair = vp != v;
     const int w = threadIdx.x % W, n2 = (threadIdx.x / W) % R1, r = threadIdx.x / (W * R1);
-    const bool live = u0 + w < g.Hv && (pair || r == 0);
+    const bool live = pair || r == 0;
     const long long cstride = g.S_c;
     C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + zoff(k)
     // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
@@ -344,7 +359,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int j = 0; j < R0 / 2; ++j) {
             const int pos = R1 * j + n2;
-            nxt[j] = (live && pos < nz) ? gcol[c * cstride + zoff(g, pos)] : mk<T>(0, 0);
+            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + zoff(g, pos)] : mk<T>(0, 0);
         }
     };
     fetch(0);
@@ -412,7 +427,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
             for (int j = 0; 2 * j < R0; ++j) {
                 const int pos = R1 * j + n2;
-                if (pos < nz) gcol[c * cstride + zoff(g, pos)] = x[j];
+                if (FZ || pos < nz) gcol[c * cstride + zoff(g, pos)] = x[j];
             }
         }
     }
