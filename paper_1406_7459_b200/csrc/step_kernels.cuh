@@ -44,6 +44,8 @@ template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int W = cmax(1, cmin(128 / CS, 65536 / (L * CS)));   // <= 64 KB tile: 2+ CTAs/SM
     static constexpr int NT = clampNT(W * L / regE<T>());
     static constexpr int SMEM = Plan<T, L>::S >= 2 ? W * L * CS : 0;
+    // resident CTAs per SM the register budget is sized for (shared memory permitting)
+    static constexpr int MINB = cmax(1, cmin(3, SMEM > 0 ? (200 * 1024) / SMEM : 3));
 };
 template <class T, int L> struct ZCfg {   // K3
     static constexpr int CS = sizeof(C2<T>);
@@ -177,7 +179,7 @@ __device__ __forceinline__ int yswz(int pos) {
 // of being masked per element.  FY: ny == Py/2 (power-of-two ny), so the
 // pruned first stage never meets a row >= ny and the row test disappears.
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YCfg<T, L>::NT)
+__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB)
 k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
@@ -202,7 +204,7 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
 
 // ------------------------------------------------------------------ K4
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YCfg<T, L>::NT)
+__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB)
 k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
