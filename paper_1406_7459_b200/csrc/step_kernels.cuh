@@ -38,6 +38,7 @@ template <class T, int N> struct LCfg {   // K5
     static constexpr int ROWS = cmax(1, cmin(32, 2048 / cmax(N, 1)));
     static constexpr int NT = 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
+    static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM)) : 1;
 };
 template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int CS = sizeof(C2<T>);
@@ -673,7 +674,7 @@ __device__ __forceinline__ void block_finish(const StepIO& io, const Ctl& ctl, d
 }
 
 template <class T, int N>
-__global__ void __launch_bounds__(LCfg<T, N>::NT)
+__global__ void __launch_bounds__(LCfg<T, N>::NT, LCfg<T, N>::MINB)
 k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
             T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io,
             Ctl ctl, Halo<T> hl) {
@@ -983,7 +984,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 }
 
 template <class T, int N, bool SUMS>
-__global__ void __launch_bounds__(LCfg<T, N>::NT)
+__global__ void __launch_bounds__(LCfg<T, N>::NT, LCfg<T, N>::MINB)
 k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
               T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
               Halo<T> hl) {
