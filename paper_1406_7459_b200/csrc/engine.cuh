@@ -33,6 +33,10 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr double kMu0 = 4.0e-7 * kPi;                       // constants.hpp:9
 constexpr double kRadToDegPerNs = 180.0 / kPi * 1e-9;       // dynamics.hpp:34
 constexpr int kMaxL = 2048;
+// Pipelined persistent K1 (cp.async staging).  Measured on B200 at
+// 512x512x64 f32 it is not faster than the plain K1 (0.33 vs 0.27 ms at 232
+// registers); kept selectable for further tuning.
+constexpr bool kUseK1Pipe = false;
 
 inline int next_pow2(int n) { int p = 1; while (p < n) p <<= 1; return p; }
 inline int padded_size(int n) { return next_pow2(2 * n); }  // demag.hpp:24
@@ -235,6 +239,8 @@ private:
     int* h_err_ = nullptr;                     // pinned
     T* h_stage_ = nullptr;                     // pinned 3N staging
     long long k5_blocks_ = 1;
+    bool k1_pipe_ = false;                     // pipelined persistent K1 usable for this grid
+    int k1_grid_ = 1, k1_smem_ = 0;
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     static constexpr int kMaxChunk = 256;
 

@@ -140,6 +140,20 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         // shared-memory opt-in for the instantiations this grid uses
         with_pow2(geo_.N, [&]<int L>() {
             set_smem<T>((const void*)k_r2c_x<T, L>, XCfg<T, L>::SMEM);
+            // pipelined K1: persistent grid sized by occupancy
+            k1_pipe_ = kUseK1Pipe && L >= 2 && g.nx % 2 == 0 && (geo_.ncell * (long long)sizeof(T)) % 16 == 0;
+            if constexpr (L >= 2) if (k1_pipe_) {
+                const int sm_bytes = XCfg<T, L>::SMEM + 2 * XCfg<T, L>::ROWS * L * (int)sizeof(T);
+                set_smem<T>((const void*)k_r2c_x_pipe<T, L>, sm_bytes);
+                int per_sm = 0, nsm = 0;
+                ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r2c_x_pipe<T, L>, XCfg<T, L>::NT,
+                                                                 sm_bytes),
+                   "occupancy");
+                ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_), "attr");
+                const long long tiles = 3 * ((nrows + XCfg<T, L>::ROWS - 1) / XCfg<T, L>::ROWS);
+                k1_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per_sm) * nsm);
+                k1_smem_ = sm_bytes;
+            }
             set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM);
@@ -317,8 +331,13 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev) {
     const long long nrows = (long long)geo_.ny * geo_.nz;
     with_pow2(geo_.N, [&]<int L>() {
         using CF = XCfg<T, L>;
-        dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
-        k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+        if (k1_pipe_) {
+            if constexpr (L >= 2)
+                k_r2c_x_pipe<T, L><<<k1_grid_, CF::NT, k1_smem_, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+        } else {
+            dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
+            k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+        }
     });
     if (ev) ck(cudaEventRecord(ev[1], stream_), "event");
     if (stop_after_ == 1) return;

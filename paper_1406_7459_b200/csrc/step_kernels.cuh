@@ -137,26 +137,39 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
     }
     __syncthreads();
     // Real-to-complex post-process on pairs (k, N-k): X[k] = E + W^k O,
-    // X[N-k] = conj(E - W^k O).  Item e -> (k = e % (N/2), row = e / (N/2));
-    // the k = 0 item also emits the self-paired k = N/2.
-    auto post = [&](int col, int k) {
+    // X[N-k] = conj(E - W^k O).  A thread owns pair index k (its twiddle is
+    // loaded once) across all ROWS rows; the k = 0 owner also emits the
+    // self-paired k = N/2.
+    auto post = [&](int col, int k, C2<T> w) {
         const C2<T> zk = sm[col * LP + xpad<T>(k & (N - 1))];
         const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>((N - k) & (N - 1))]);
         const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
         const C2<T> d = csub<T>(zk, zn);
         const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
-        const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));        // W_Px^k
         const C2<T> wo = cmul<T>(w, O);
         C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
         dst[k] = cadd<T>(E, wo);
         if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
     };
     constexpr int HP = N / 2 > 0 ? N / 2 : 1;
-    for (int e = threadIdx.x; e < ROWS * HP; e += NT) {
-        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
-        if (row0 + col >= nrows) continue;
-        post(col, k);
-        if (k == 0 && N > 1) post(col, N / 2);
+    const int rows = (int)(nrows - row0 < ROWS ? nrows - row0 : ROWS);
+    if constexpr (HP >= NT) {
+        for (int k = threadIdx.x; k < HP; k += NT) {
+            const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));     // W_Px^k
+            const C2<T> wh = __ldg(tw + (N / 2) * (TWN / (2 * N)));
+#pragma unroll 4
+            for (int col = 0; col < rows; ++col) {
+                post(col, N / 2 > 0 ? k : 0, w);
+                if (k == 0 && N > 1) post(col, N / 2, wh);
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < ROWS * HP; e += NT) {
+            const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+            if (col >= rows) continue;
+            post(col, k, __ldg(tw + k * (TWN / (2 * N))));
+            if (k == 0 && N > 1) post(col, N / 2, __ldg(tw + (N / 2) * (TWN / (2 * N))));
+        }
     }
 }
 
@@ -172,6 +185,86 @@ __device__ __forceinline__ int yswz(int pos) {
     constexpr int RL = S == 3 ? Plan<T, L>::R2 : S == 2 ? Plan<T, L>::R1 : 1;
     if constexpr (kYSwizzle && W * (int)sizeof(C2<T>) == 64 && S >= 2) return pos ^ ((pos / RL) & 1);
     else return pos;
+}
+
+// ---------------------------------------------------- async copy helpers
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory"); }
+
+// K1, pipelined persistent form: each CTA walks (component, row group)
+// tiles; the ROWS consecutive M rows of the NEXT tile (one contiguous span)
+// stream into a shared staging buffer with cp.async while the current tile
+// is transformed, so HBM latency overlaps the FFT instead of stalling it.
+// Needs nx even and 16-byte aligned component planes (checked on the host).
+template <class T, int N>
+__global__ void __launch_bounds__(XCfg<T, N>::NT, 3)
+k_r2c_x_pipe(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+    using CF = XCfg<T, N>;
+    constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>();
+    constexpr int VEC = 16 / sizeof(T);
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
+    T* stage[2] = {reinterpret_cast<T*>(sm + ROWS * LP), reinterpret_cast<T*>(sm + ROWS * LP) + ROWS * N};
+    const long long nrows = (long long)g.ny * g.nz;
+    const int ngroups = (int)((nrows + ROWS - 1) / ROWS);
+    const int ntiles = 3 * ngroups;
+    const int nx = g.nx;
+    auto fetch = [&](int t, T* buf) {
+        const int comp = t / ngroups, grp = t % ngroups;
+        const long long r0 = (long long)grp * ROWS;
+        const long long rows = nrows - r0 < ROWS ? nrows - r0 : ROWS;
+        const T* src = M + comp * g.ncell + r0 * nx;
+        const int chunks = (int)(rows * nx / VEC);
+        for (int q = threadIdx.x; q < chunks; q += NT) cp_async16(buf + q * VEC, src + q * VEC);
+    };
+    int t = blockIdx.x;
+    if (t < ntiles) fetch(t, stage[0]);
+    cp_commit();
+    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
+        if (t + (int)gridDim.x < ntiles) fetch(t + gridDim.x, stage[(it + 1) & 1]);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const T* in = stage[it & 1];
+        const int comp = t / ngroups;
+        const long long row0 = (long long)(t % ngroups) * ROWS;
+        auto ld0 = [&](int col, int pos) -> C2<T> {
+            const int i0 = 2 * pos;
+            if (row0 + col >= nrows || i0 >= nx) return mk<T>(0, 0);
+            return *reinterpret_cast<const C2<T>*>(in + col * nx + i0);
+        };
+        auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
+        auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
+        fft_forward<T, N, ROWS, NT, false, false, true, true, true>(ld0, lds, sts, sts, tw);
+        __syncthreads();
+        auto post = [&](int col, int k) {
+            const C2<T> zk = sm[col * LP + xpad<T>(k & (N - 1))];
+            const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>((N - k) & (N - 1))]);
+            const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
+            const C2<T> d = csub<T>(zk, zn);
+            const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);
+            const C2<T> w = __ldg(tw + k * (TWN / (2 * N)));
+            const C2<T> wo = cmul<T>(w, O);
+            C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
+            dst[k] = cadd<T>(E, wo);
+            if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
+        };
+        constexpr int HP = N / 2;
+        for (int e = threadIdx.x; e < ROWS * HP; e += NT) {
+            const int col = e / HP, k = e % HP;
+            if (row0 + col >= nrows) continue;
+            post(col, k);
+            if (k == 0) post(col, N / 2);
+        }
+        __syncthreads();   // staging buffer and work tile are reused next iteration
+    }
+    cp_wait<0>();
 }
 
 // ------------------------------------------------------------------ K2
