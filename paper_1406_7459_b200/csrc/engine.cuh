@@ -240,6 +240,7 @@ private:
     T* h_stage_ = nullptr;                     // pinned 3N staging
     long long k5_blocks_ = 1;
     bool k1_pipe_ = false;                     // pipelined persistent K1 usable for this grid
+    bool small_x_ = false;                     // few rows: small-CTA variants of K1 / K5
     int k1_grid_ = 1, k1_smem_ = 0;
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     static constexpr int kMaxChunk = 256;

@@ -158,6 +158,11 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM);
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
+            // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
+            small_x_ = L >= 2 && L <= 256 && k5_blocks_ < 2 * nsm && g.nx % V16<T>::V == 0;
+            if (small_x_) k5_blocks_ = nrows;
         });
         with_pow2(Py_, [&]<int L>() {
             set_smem<T>((const void*)k_fft_y_fwd<T, L, true>, YCfg<T, L>::SMEM);
@@ -334,6 +339,12 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev) {
         if (k1_pipe_) {
             if constexpr (L >= 2)
                 k_r2c_x_pipe<T, L><<<k1_grid_, CF::NT, k1_smem_, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+        } else if (small_x_) {
+            if constexpr (L >= 2 && L <= 256) {
+                using CS = XCfg<T, L, 2>;
+                dim3 grid((unsigned)((nrows + 1) / 2), 3);
+                k_r2c_x<T, L, 2><<<grid, CS::NT, CS::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+            }
         } else {
             dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
             k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
@@ -397,6 +408,18 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
+        if constexpr (L >= 2 && L <= 256) {
+            if (small_x_) {   // one row per CTA (few-row grids such as SP4)
+                using CS = LCfg<T, L, 1>;
+                if (io.sums)
+                    k_c2r_x_llg_v<T, L, true, 1><<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(
+                        geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+                else
+                    k_c2r_x_llg_v<T, L, false, 1><<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(
+                        geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+                return;
+            }
+        }
         if (geo_.nx % V16<T>::V == 0 && io.sums)
             k_c2r_x_llg_v<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io,
                                                                             ctl, hl);

@@ -28,15 +28,17 @@ template <class T> __device__ __forceinline__ int xpad(int pos) { return pos + (
 template <class T, int L> constexpr int xpitch() { return L + (L >> padShift<T>()) + 1; }
 
 // -------------------------------------------------------------- configs
-template <class T, int N> struct XCfg {   // K1
+// RS > 0: small-grid variant with RS rows per CTA, so grids of a few dozen
+// rows (SP4: 32) still spread over the SMs instead of running 1-3 CTAs.
+template <class T, int N, int RS = 0> struct XCfg {   // K1
     static constexpr int E = regE<T>();
-    static constexpr int ROWS = cmax(1, cmin(64, 128 * E / N));   // small CTAs: many independent phase schedules per SM
-    static constexpr int NT = clampNT(cmax(128, ROWS * N / E));
+    static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(64, 128 * E / N));   // small CTAs: many phase schedules per SM
+    static constexpr int NT = RS > 0 ? clampNT(ROWS * N / E) : clampNT(cmax(128, ROWS * N / E));
     static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
 };
-template <class T, int N> struct LCfg {   // K5
-    static constexpr int ROWS = cmax(1, cmin(32, 2048 / cmax(N, 1)));
-    static constexpr int NT = 256;
+template <class T, int N, int RS = 0> struct LCfg {   // K5
+    static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(32, 2048 / cmax(N, 1)));
+    static constexpr int NT = RS > 0 ? 64 : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
     static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM)) : 1;
 };
@@ -102,10 +104,10 @@ __device__ __forceinline__ bool halted(const Ctl& c) {
 }
 
 // ------------------------------------------------------------------ K1
-template <class T, int N>
-__global__ void __launch_bounds__(XCfg<T, N>::NT)
+template <class T, int N, int RS = 0>
+__global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
 k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
-    using CF = XCfg<T, N>;
+    using CF = XCfg<T, N, RS>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>();
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1076,12 +1078,12 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
     }
 }
 
-template <class T, int N, bool SUMS>
-__global__ void __launch_bounds__(LCfg<T, N>::NT, LCfg<T, N>::MINB)
+template <class T, int N, bool SUMS, int RS = 0>
+__global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
 k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
               T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
               Halo<T> hl) {
-    using CF = LCfg<T, N>;
+    using CF = LCfg<T, N, RS>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
     constexpr int V = V16<T>::V;
     if (halted(ctl)) return;

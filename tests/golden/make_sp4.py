@@ -1,0 +1,58 @@
+#!/usr/bin/env python3
+"""Regenerates tests/golden/sp4_*.npz from the REFERENCE itself (oracle/_ref,
+built from /root/reference/proj).  muMAG standard problem 4 on the 128x32x1
+grid (BASELINE configs[0]):
+
+* relax: permalloy (Ms 8e5, A 1.3e-11, Ku 0), alpha = 1, dt = 5e-14 s, from the
+  uniform (1,1,1)/sqrt3 state to the 0.01 deg/ns torque criterion
+  (dynamics::relax, sampled every 100 steps) -> the s-state;
+* field 1: from that s-state, alpha = 0.02, mu0*H = (-24.6, 4.3, 0) mT,
+  4000 steps = 200 ps, <m> every 200 steps (10 ps) (Simulation::step).
+
+Takes a few minutes on 8 host threads.
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from oracle import oracle as O  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GRID = (128, 32, 1, 500e-9 / 128, 125e-9 / 32, 3e-9)
+MU0 = 4e-7 * np.pi
+H1 = (-24.6e-3 / MU0, 4.3e-3 / MU0, 0.0)
+
+
+def main():
+    assert O.ref_available()
+    t0 = time.time()
+    spec = O.Spec(*GRID, A=1.3e-11, Ku=0.0, Ms=8e5, alpha=1.0, anisotropy=False, zeeman=False,
+                  dt=5e-14, max_steps=200000, torque_tol=0.01, sample_every=100, parallel=True,
+                  threads=os.cpu_count())
+    r = O.Ref(spec, 64)
+    u = 8e5 / np.sqrt(3.0)
+    r.set_m(np.full((3, spec.n), u))
+    conv, log = r.relax(cap=4000)
+    s_state = r.get_m()
+    rel = np.array([[s.step, s.t, s.m[0], s.m[1], s.m[2], s.torque, s.e_total] for s in log])
+    np.savez_compressed(os.path.join(HERE, "sp4_relax.npz"), samples=rel, converged=conv, s_state=s_state)
+    print("relax", conv, rel[-1, 0], rel[-1, 2:5], f"{time.time() - t0:.0f}s", flush=True)
+
+    f1 = O.Spec(*GRID, A=1.3e-11, Ku=0.0, Ms=8e5, alpha=0.02, anisotropy=False, zeeman=True, h_ext=H1,
+                dt=5e-14, parallel=True, threads=os.cpu_count())
+    r1 = O.Ref(f1, 64)
+    r1.set_m(s_state)
+    out = []
+    for blk in range(21):
+        out.append([blk * 200, *(r1.get_m().sum(axis=1) / (8e5 * f1.n))])
+        if blk < 20:
+            r1.step(200)
+    np.savez_compressed(os.path.join(HERE, "sp4_field1.npz"), samples=np.array(out))
+    print("field1 done", f"{time.time() - t0:.0f}s")
+
+
+if __name__ == "__main__":
+    main()
