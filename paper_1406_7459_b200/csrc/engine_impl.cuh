@@ -32,9 +32,15 @@ __global__ void k_fill3(T* m, long long n, T x, T y, T z) {
 }
 
 template <class T>
-static void set_smem(const void* fn, int bytes) {
+static void set_smem(const void* fn, int bytes, bool carve = true) {
     if (bytes > 48 * 1024)
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+    // Forcing the full shared-memory carveout was measured slower on B200
+    // (512x512x64 f32: K2 0.31 -> 0.39 ms, K3 0.69 -> 0.73 ms): the passes'
+    // strided column loads profit from L1.  Kept switchable.
+    constexpr bool kCarveout = false;
+    if (kCarveout && carve && bytes > 0)
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout attr");
 }
 
 template <class T>
@@ -154,9 +160,9 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
                 k1_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per_sm) * nsm);
                 k1_smem_ = sm_bytes;
             }
-            set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM);
+            set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM, false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM, false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM, false);
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
             // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
             int nsm = 148;
@@ -172,8 +178,10 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         });
         with_pow2(Pz_, [&]<int L>() {
             if constexpr (z_variant<T, L>() == 2) {
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, true>, Z2Cfg<T, L>::SMEM);
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, false>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, true, false>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, false, false>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, true, true>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, false, true>, Z2Cfg<T, L>::SMEM);
             }
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
@@ -374,10 +382,10 @@ void Engine<T>::enq_B(const Iter& it) {
         } else if constexpr (z_variant<T, L>() == 2) {
             using CF = Z2Cfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
-            if (2 * geo_.nzg == L)
-                k_fft_z_conv2<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
-            else
-                k_fft_z_conv2<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
+            const bool fz = 2 * geo_.nzg == L, multi = geo_.G > 1;
+            auto* k = fz ? (multi ? k_fft_z_conv2<T, L, true, true> : k_fft_z_conv2<T, L, true, false>)
+                         : (multi ? k_fft_z_conv2<T, L, false, true> : k_fft_z_conv2<T, L, false, false>);
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
         } else {
             using CF = ZCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);

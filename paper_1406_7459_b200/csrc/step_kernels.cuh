@@ -82,6 +82,12 @@ __device__ __forceinline__ long long zoff(const Geo& g, int k) {
     if (g.G == 1) return (long long)k * g.S_k;
     return (long long)(k / g.nz) * g.S_blk + (long long)(k % g.nz) * g.S_k;
 }
+// Same with the single-GPU case resolved at compile time (no division code).
+template <bool MULTI>
+__device__ __forceinline__ long long zoff_t(const Geo& g, int k) {
+    if constexpr (!MULTI) return (long long)k * g.S_k;
+    else return (long long)(k / g.nz) * g.S_blk + (long long)(k % g.nz) * g.S_k;
+}
 // One-plane M halos below / above the slab ([3][ny][nx] each; null at the
 // global boundary or on a single GPU).
 template <class T> struct Halo { const T* lo; const T* hi; };
@@ -395,6 +401,27 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
 // kp points at the bin's six interleaved components (Kt layout [v][w][u][6]),
 // read as three 8/16-byte vectors.
 template <class T>
+struct KBin { C2<T> k01, k23, k45; };
+template <class T>
+__device__ __forceinline__ KBin<T> kload(const T* __restrict__ kp) {
+    KBin<T> k;
+    k.k01 = __ldg(reinterpret_cast<const C2<T>*>(kp));
+    k.k23 = __ldg(reinterpret_cast<const C2<T>*>(kp) + 1);
+    k.k45 = __ldg(reinterpret_cast<const C2<T>*>(kp) + 2);
+    return k;
+}
+template <class T>
+__device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const KBin<T>& kb, T sy, T sz) {
+    const C2<T> k01 = kb.k01, k23 = kb.k23, k45 = kb.k45;
+    const T kxx = k01.x, kyy = k01.y, kzz = k23.x;
+    const T cxy = sy * k23.y, cxz = sz * k45.x;
+    const T cyz = sy * sz * k45.y;
+    const C2<T> a = mx, b = my, c = mz;
+    mx = mk<T>(kxx * a.x + cxy * b.x + cxz * c.x, kxx * a.y + cxy * b.y + cxz * c.y);
+    my = mk<T>(cxy * a.x + kyy * b.x + cyz * c.x, cxy * a.y + kyy * b.y + cyz * c.y);
+    mz = mk<T>(cxz * a.x + cyz * b.x + kzz * c.x, cxz * a.y + cyz * b.y + kzz * c.y);
+}
+template <class T>
 __device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* __restrict__ kp, T sy, T sz) {
     const C2<T> k01 = __ldg(reinterpret_cast<const C2<T>*>(kp));
     const C2<T> k23 = __ldg(reinterpret_cast<const C2<T>*>(kp) + 1);
@@ -422,12 +449,17 @@ template <class T, int L> struct Z2Cfg {
     static constexpr int NCOL = 6 * W;
     static constexpr int NT = W * R1 * 2;
     static constexpr int SMEM = NCOL * L * CS;
+    // resident CTAs per SM the register budget is sized for (shared memory permitting)
+    // tensor bins loaded one phase ahead (register budget: R1 <= 8 only)
+    static constexpr bool KPRE = R1 <= 8;
+    static constexpr int MINB = KPRE ? cmax(1, cmin(2, (200 * 1024) / SMEM)) : 1;
 };
 
 // FZ: nz == Pz/2, so the pruned first/last stages never meet a plane >= nz.
 // Padding x-bins (>= Hv, inside the block pitch) are computed, not masked.
-template <class T, int L, bool FZ>
-__global__ void __launch_bounds__(Z2Cfg<T, L>::NT)
+// MULTI: z-slab decomposition (planes spread over the receive blocks).
+template <class T, int L, bool FZ, bool MULTI = false>
+__global__ void __launch_bounds__(Z2Cfg<T, L>::NT, Z2Cfg<T, L>::MINB)
 k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
               const int* __restrict__ ybuf, Ctl ctl) {
     using CF = Z2Cfg<T, L>;
@@ -448,16 +480,17 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + r * W + w;
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
-    // All 3*R0/2 HBM loads of the thread are issued before any arithmetic.
+    // Software pipeline over the three components: the loads of component
+    // c+1 are in flight while component c is transformed.  (A persistent
+    // variant that also prefetched the next tile measured slower on B200:
+    // 0.88 vs 0.69 ms at 512x512x64 f32, the tensor loads lost their overlap.)
     {
-    // software pipeline over the three components: the loads of component
-    // c+1 are in flight while component c is transformed.
     C2<T> nxt[R0 / 2];
     auto fetch = [&](int c) {
 #pragma unroll
         for (int j = 0; j < R0 / 2; ++j) {
             const int pos = R1 * j + n2;
-            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + zoff(g, pos)] : mk<T>(0, 0);
+            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + zoff_t<MULTI>(g, pos)] : mk<T>(0, 0);
         }
     };
     fetch(0);
@@ -477,11 +510,24 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
         for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * 2 * W] = x[k];
     }
     }
-    __syncthreads();
-    // ---- stage 1 + tensor product + inverse stage 1, in registers
+    // ---- stage 1 + tensor product + inverse stage 1, in registers.  The
+    // tensor bins of iteration it are loaded one phase ahead (before the
+    // barrier for it = 0, after the product of it - 1 otherwise), so their
+    // HBM latency overlaps the shared-memory gather and the stage-1 DFTs.
     const int Hz = L / 2 + 1;
     const T sy = r ? T(-1) : T(1);
-#pragma unroll 1
+    const T* kb = Kt + ((long long)v * Hz * Wb + u0 + w) * 6;
+    KBin<T> kv[CF::KPRE ? R1 : 1];
+    auto kfetch = [&](int it) {
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            const int f = n2 + R1 * it + R0 * k1;
+            kv[k1] = kload<T>(kb + (long long)(2 * f > L ? L - f : f) * Wb * 6);
+        }
+    };
+    if constexpr (CF::KPRE) if (live) kfetch(0);
+    __syncthreads();
+#pragma unroll
     for (int it = 0; it < R0 / R1; ++it) {
         const int k0 = n2 + R1 * it;
         C2<T> y[3][R1];
@@ -492,14 +538,17 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int c = 0; c < 3; ++c) dft<T, R1, false>(y[c]);
         if (live) {
-            const T* kb = Kt + ((long long)v * Hz * Wb + u0 + w) * 6;
 #pragma unroll
             for (int k1 = 0; k1 < R1; ++k1) {
                 const int f = k0 + R0 * k1;
                 const bool hi = 2 * f > L;
-                kmul<T>(y[0][k1], y[1][k1], y[2][k1], kb + (long long)(hi ? L - f : f) * Wb * 6, sy,
-                        hi ? T(-1) : T(1));
+                if constexpr (CF::KPRE)
+                    kmul<T>(y[0][k1], y[1][k1], y[2][k1], kv[k1], sy, hi ? T(-1) : T(1));
+                else
+                    kmul<T>(y[0][k1], y[1][k1], y[2][k1], kb + (long long)(hi ? L - f : f) * Wb * 6, sy,
+                            hi ? T(-1) : T(1));
             }
+            if constexpr (CF::KPRE) if (it + 1 < R0 / R1) kfetch(it + 1);
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) dft<T, R1, true>(y[c]);
@@ -525,7 +574,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
             for (int j = 0; 2 * j < R0; ++j) {
                 const int pos = R1 * j + n2;
-                if (FZ || pos < nz) gcol[c * cstride + zoff(g, pos)] = x[j];
+                if (FZ || pos < nz) gcol[c * cstride + zoff_t<MULTI>(g, pos)] = x[j];
             }
         }
     }
