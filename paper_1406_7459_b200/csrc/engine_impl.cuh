@@ -169,6 +169,16 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
             small_x_ = L >= 2 && L <= 256 && k5_blocks_ < 2 * nsm && g.nx % V16<T>::V == 0;
             if (small_x_) k5_blocks_ = nrows;
+            // L2 prefetch distances: one resident wave of CTAs
+            int per1 = 0, per5 = 0;
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_r2c_x<T, L>, XCfg<T, L>::NT,
+                                                             XCfg<T, L>::SMEM), "occupancy");
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per5, k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::NT,
+                                                             LCfg<T, L>::SMEM), "occupancy");
+            geo_.pf1 = per1 * nsm;
+            geo_.pf5 = per5 * nsm;
+            geo_.pfm = small_x_ ? 0 : kL2PrefetchMask;
+            if (const char* e = getenv("MFD_PF_MASK")) geo_.pfm = atoi(e);   // tuning override
         });
         with_pow2(Py_, [&]<int L>() {
             set_smem<T>((const void*)k_fft_y_fwd<T, L, true>, YCfg<T, L>::SMEM);

@@ -76,7 +76,18 @@ struct Geo {
     int nzg, k0;          // global planes, first plane of the slab
     int G, ublk, Wb, Hv;  // ranks, this rank's x-bin block, block width, valid bins in it
     long long S_blk, S_c, S_k;   // B strides: block, component, plane (row stride Wb)
+    int pf1, pf5;         // L2 prefetch distance of K1 / K5 in CTAs (~resident CTAs; 0 = off)
+    int pfm;              // prefetch mask: 1 K1 ahead, 2 K5 own M rows, 4 K5 spectrum ahead
 };
+
+// Asynchronous L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch, TMA
+// unit: no registers, no shared memory).  Trimmed inward to 16-byte bounds.
+__device__ __forceinline__ void l2_prefetch(const void* p, long long bytes) {
+    const unsigned long long a = (reinterpret_cast<unsigned long long>(p) + 15) & ~15ull;
+    const unsigned long long e = (reinterpret_cast<unsigned long long>(p) + bytes) & ~15ull;
+    if (e <= a) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
 // z offset of global plane k in the receive-side layout (rank k / nz, plane k % nz).
 __device__ __forceinline__ long long zoff(const Geo& g, int k) {
     if (g.G == 1) return (long long)k * g.S_k;
@@ -124,6 +135,15 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
     const T* Mc = M + comp * g.ncell;
     const int nx = g.nx;
     const bool even = (nx & 1) == 0;
+    // rows of the CTA ~one resident wave later: in L2 by the time it starts
+    if ((g.pfm & 1) && threadIdx.x == 0) {
+        const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + g.pf1;
+        if (lin < (long long)gridDim.x * gridDim.y) {
+            const long long r1 = (lin % gridDim.x) * ROWS;
+            const long long nr = nrows - r1 < ROWS ? nrows - r1 : ROWS;
+            l2_prefetch(M + (lin / gridDim.x) * g.ncell + r1 * nx, nr * nx * (long long)sizeof(T));
+        }
+    }
 
     auto ld0 = [&](int col, int pos) -> C2<T> {
         const long long row = row0 + col;
@@ -1140,6 +1160,26 @@ k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const long long nrows = (long long)g.ny * g.nz;
     const long long row0 = (long long)blockIdx.x * ROWS;
+    if ((g.pfm & 6) && threadIdx.x < 3) {
+        // this CTA's M rows with their y / z neighbour rows (read by the
+        // epilogue, after the inverse FFT) ...
+        const int c = threadIdx.x;
+        if (g.pfm & 2) {
+        const T* Mc = M + c * g.ncell;
+        const long long nx = g.nx, ny = g.ny;
+        const long long ra = row0 - 1 > 0 ? row0 - 1 : 0, rb = row0 + ROWS + 1 < nrows ? row0 + ROWS + 1 : nrows;
+        l2_prefetch(Mc + ra * nx, (rb - ra) * nx * (long long)sizeof(T));
+        const long long re = row0 + ROWS < nrows ? row0 + ROWS : nrows;
+        if (row0 >= ny) l2_prefetch(Mc + (row0 - ny) * nx, (re - row0) * nx * (long long)sizeof(T));
+        if (re + ny <= nrows) l2_prefetch(Mc + (row0 + ny) * nx, (re - row0) * nx * (long long)sizeof(T));
+        }
+        // ... and the spectrum rows of the CTA one resident wave later
+        const long long r1 = row0 + (long long)g.pf5 * ROWS;
+        if ((g.pfm & 4) && r1 < nrows) {
+            const long long nr = nrows - r1 < ROWS ? nrows - r1 : ROWS;
+            l2_prefetch(A + ((long long)c * nrows + r1) * g.Hp, nr * g.Hp * (long long)sizeof(C2<T>));
+        }
+    }
     // C2R pre-process over pairs (k, N-k): item e -> (k = e % (N/2), column
     // = e / (N/2)); the k = 0 item also carries the self-paired k = N/2.  All
     // HBM loads of the thread are issued before any use (compile-time trip
