@@ -345,3 +345,56 @@ def rel_linf(a: np.ndarray, b: np.ndarray) -> float:
     d = np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)))
     r = np.max(np.abs(b))
     return float(d / r) if r > 0 else float(d)
+
+
+# ---- host formats: the reference's own
+# parseConfig / formatConfig, io::writeFieldDump / readFieldDump,
+# io::writeTrajectoryCsv and makeVortexState, for byte-level parity tests.
+def ref_config_format(text: str):
+    """parseConfig + formatConfig (config.cpp:76-276) -> (rc, canonical text or
+    ConfigError text, applied-default lines); rc 0 ok, 7 ConfigError."""
+    lib = _load(REF_SO)
+    out, dflt = C.create_string_buffer(1 << 16), C.create_string_buffer(1 << 16)
+    rc = lib.ref_config_format(text.encode(), out, C.c_size_t(len(out)), dflt, C.c_size_t(len(dflt)))
+    return rc, out.value.decode(), [l for l in dflt.value.decode().split("\n") if l]
+
+
+def ref_last_error() -> str:
+    lib = _load(REF_SO)
+    lib.ref_last_error.restype = C.c_char_p
+    return lib.ref_last_error().decode()
+
+
+def ref_dump_write(path: str, m: np.ndarray, nx, ny, nz, dx, dy, dz, Ms, precision_bits=64) -> int:
+    m = np.ascontiguousarray(m, dtype=np.float64).reshape(3, -1)
+    x, y, z = (np.ascontiguousarray(m[i]) for i in range(3))
+    return _load(REF_SO).ref_dump_write(str(path).encode(), nx, ny, nz, C.c_double(dx), C.c_double(dy),
+                                        C.c_double(dz), C.c_double(Ms), precision_bits, _ptr(x), _ptr(y), _ptr(z))
+
+
+def ref_dump_read(path: str):
+    """-> (rc, header [nx, ny, nz, dx, dy, dz, Ms, precision_bits], M 3 x N or None)."""
+    lib = _load(REF_SO)
+    hdr = np.zeros(8)
+    rc = lib.ref_dump_read(str(path).encode(), _ptr(hdr), None, C.c_longlong(0))
+    if rc != 0:
+        return rc, None, None
+    n = int(hdr[0] * hdr[1] * hdr[2])
+    m = np.zeros(3 * n)
+    rc = lib.ref_dump_read(str(path).encode(), _ptr(hdr), _ptr(m), C.c_longlong(3 * n))
+    return rc, hdr, m.reshape(3, n)
+
+
+def ref_trajectory_csv(path: str, rows: np.ndarray) -> int:
+    """rows: n x 11 {step, t, mx, my, mz, E_exch, E_anis, E_demag, E_zeeman, E_total, torque}."""
+    rows = np.ascontiguousarray(rows, dtype=np.float64)
+    return _load(REF_SO).ref_trajectory_csv(str(path).encode(), _ptr(rows), C.c_long(len(rows)))
+
+
+def ref_vortex_state(precision_bits, nx, ny, nz, dx, dy, dz, axis: int, Ms: float) -> np.ndarray:
+    """makeVortexState<T> (state.hpp:83-108) widened to f64, 3 x N."""
+    m = np.zeros(3 * nx * ny * nz)
+    rc = _load(REF_SO).ref_vortex_state(precision_bits, nx, ny, nz, C.c_double(dx), C.c_double(dy),
+                                        C.c_double(dz), axis, C.c_double(Ms), _ptr(m))
+    assert rc == 0, ref_last_error()
+    return m.reshape(3, -1)

@@ -15,6 +15,10 @@
 //   ref_tensor_entry    -> newell::demagTensorEntry      (newell.cpp:188-209)
 //   ref_direct_demag    -> oracle::directDemag           (oracle.hpp:26-70)
 //   ref_spectrum_octant -> demag::precomputeSpectrum     (demag.hpp:105-119)
+//   ref_config_format   -> parseConfig + formatConfig    (config.cpp:76-276)
+//   ref_dump_write/read -> io::writeFieldDump / readFieldDump (io.cpp:18-100)
+//   ref_trajectory_csv  -> io::writeTrajectoryCsv        (io.cpp:102-117)
+//   ref_vortex_state    -> makeVortexState               (state.hpp:83-108)
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -23,6 +27,8 @@
 #include <vector>
 
 #include "magfd/backend.hpp"
+#include "magfd/config.hpp"
+#include "magfd/io.hpp"
 #include "magfd/demag.hpp"
 #include "magfd/dynamics.hpp"
 #include "magfd/fields.hpp"
@@ -365,6 +371,111 @@ double ref_stability_dt_limit(double A, double Ms, double alpha, double gamma, d
     m.alpha = alpha;
     m.gamma = gamma;
     return dynamics::stabilityDtLimit(m, Grid(1, 1, 1, dx, dy, dz));
+}
+
+// parseConfig(text, &defaults) -> formatConfig.  Returns 0 (out = canonical
+// text, defaults = applied-default lines) or 7 (out = ConfigError text).
+static void put(const std::string& s, char* out, size_t cap) {
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(out, s.data(), n);
+    out[n] = 0;
+}
+int ref_config_format(const char* text, char* out, size_t cap, char* defaults, size_t dcap) {
+    try {
+        std::vector<std::string> d;
+        const SimSpec spec = parseConfig(text, &d);
+        put(formatConfig(spec), out, cap);
+        std::string all;
+        for (const auto& l : d) all += l + "\n";
+        put(all, defaults, dcap);
+        return 0;
+    } catch (const ConfigError& e) {
+        put(e.what(), out, cap);
+        return 7;
+    }
+}
+
+int ref_dump_write(const char* path, int nx, int ny, int nz, double dx, double dy, double dz, double Ms, int prec,
+                   const double* mx, const double* my, const double* mz) {
+    try {
+        Grid g(nx, ny, nz, dx, dy, dz);
+        VectorField<double> M(g);
+        for (std::size_t c = 0; c < M.size(); ++c) M.set(c, {mx[c], my[c], mz[c]});
+        io::writeFieldDump(path, M, Ms, prec == 32 ? Precision::f32 : Precision::f64);
+        return 0;
+    } catch (const io::IoError& e) {
+        g_err = e.what();
+        return 8;
+    }
+}
+
+// hdr = {nx, ny, nz, dx, dy, dz, Ms, precision_bits}; m = 3 x N (may be null: header only)
+int ref_dump_read(const char* path, double* hdr, double* m, long long cap) {
+    try {
+        const io::FieldDump d = io::readFieldDump(path);
+        const Grid& g = d.grid;
+        const double h[8] = {(double)g.nx, (double)g.ny, (double)g.nz, g.dx, g.dy, g.dz, d.Ms,
+                             d.precision == Precision::f32 ? 32.0 : 64.0};
+        std::memcpy(hdr, h, sizeof h);
+        const long long n = (long long)g.cellCount();
+        if (m && cap >= 3 * n)
+            for (long long c = 0; c < n; ++c) {
+                m[c] = d.M.x[c];
+                m[c + n] = d.M.y[c];
+                m[c + 2 * n] = d.M.z[c];
+            }
+        return 0;
+    } catch (const io::IoError& e) {
+        g_err = e.what();
+        return 8;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// rows: n x 11 {step, t, mx, my, mz, E_exch, E_anis, E_demag, E_zeeman, E_total, torque}
+int ref_trajectory_csv(const char* path, const double* rows, long n) {
+    try {
+        std::vector<dynamics::TrajectorySample> log(n);
+        for (long r = 0; r < n; ++r) {
+            const double* x = rows + 11 * r;
+            auto& s = log[r];
+            s.step = (long)x[0];
+            s.t = x[1];
+            s.m = {x[2], x[3], x[4]};
+            s.energy.exchange = x[5];
+            s.energy.anisotropy = x[6];
+            s.energy.demag = x[7];
+            s.energy.zeeman = x[8];
+            s.energy.total = x[9];
+            s.maxTorqueDegPerNs = x[10];
+        }
+        io::writeTrajectoryCsv(path, log);
+        return 0;
+    } catch (const io::IoError& e) {
+        g_err = e.what();
+        return 8;
+    }
+}
+
+// makeVortexState<T>(grid, axis, Ms) -> 3 x N (as double)
+int ref_vortex_state(int precision_bits, int nx, int ny, int nz, double dx, double dy, double dz, int axis, double Ms,
+                     double* m) {
+    return guard([&] {
+        Grid g(nx, ny, nz, dx, dy, dz);
+        const SignedAxis a = static_cast<SignedAxis>(axis);
+        const std::size_t n = g.cellCount();
+        auto emit = [&](const auto& st) {
+            for (std::size_t c = 0; c < n; ++c) {
+                m[c] = (double)st.M.x[c];
+                m[c + n] = (double)st.M.y[c];
+                m[c + 2 * n] = (double)st.M.z[c];
+            }
+        };
+        if (precision_bits == 32) emit(makeVortexState<float>(g, a, Ms));
+        else emit(makeVortexState<double>(g, a, Ms));
+    });
 }
 
 } // extern "C"

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "engine.cuh"
+#include "../../include/mfd_host.h"
 
 struct mfd_ctx {
     std::unique_ptr<mfd::EngineBase> eng;
@@ -124,6 +125,9 @@ mfd_status mfd_set_m_uniform(mfd_ctx* c, const double dir[3]) {
             throw mfd::Error(MFD_EINVAL, "makeUniformState: direction must be a unit vector");
         ENG(c)->set_uniform(dir);
     });
+}
+mfd_status mfd_set_m_vortex(mfd_ctx* c, int axis) {
+    return guard(c, [&] { ENG(c)->set_vortex(axis); });
 }
 mfd_status mfd_set_time(mfd_ctx* c, double t, long step) {
     return guard(c, [&] {

@@ -134,6 +134,7 @@ public:
     virtual void get_m(double*, double*, double*) = 0;
     virtual void get_m32(float*, float*, float*) = 0;
     virtual void set_uniform(const double dir[3]) = 0;
+    virtual void set_vortex(int axis) = 0;
     virtual void field(int which, double*, double*, double*) = 0;
     virtual void step(long n, double* last, double* all) = 0;
     virtual void step_async(long n) = 0;
@@ -173,6 +174,7 @@ public:
     void get_m(double* x, double* y, double* z) override;
     void get_m32(float* x, float* y, float* z) override;
     void set_uniform(const double dir[3]) override;
+    void set_vortex(int axis) override;
     void field(int which, double* x, double* y, double* z) override;
     void step(long n, double* last, double* all) override;
     void step_async(long n) override;

@@ -31,6 +31,42 @@ __global__ void k_fill3(T* m, long long n, T x, T y, T z) {
     m[i + 2 * n] = z;
 }
 
+// makeVortexState (state.hpp:83-108) per cell, fp64 in the reference's
+// operation order with explicit round-to-nearest ops (no contraction), so the
+// cast to T is bitwise the host result.  Global plane index k0 + k.
+template <class T>
+__global__ void k_vortex(T* m, int nx, int ny, int nz, int nzg, int k0, double dx, double dy, double dz, double ax,
+                         double ay, double az, double Ms) {
+    const long long n = (long long)nx * ny * nz;
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const int i = (int)(c % nx), j = (int)((c / nx) % ny), k = k0 + (int)(c / ((long long)nx * ny));
+    const bool along_x = ax != 0, along_y = ay != 0;
+    const double d1 = along_x ? dy : dx, d2 = (along_x || along_y) ? dz : dy;
+    const double core = fmin(d1, d2);
+    const double cx = __dmul_rn(0.5, (double)(nx - 1)), cy = __dmul_rn(0.5, (double)(ny - 1)),
+                 cz = __dmul_rn(0.5, (double)(nzg - 1));
+    const double rx = __dmul_rn(__dsub_rn((double)i, cx), dx), ry = __dmul_rn(__dsub_rn((double)j, cy), dy),
+                 rz = __dmul_rn(__dsub_rn((double)k, cz), dz);
+    const double ra = __dadd_rn(__dadd_rn(__dmul_rn(rx, ax), __dmul_rn(ry, ay)), __dmul_rn(rz, az));
+    const double px = __dsub_rn(rx, __dmul_rn(ra, ax)), py = __dsub_rn(ry, __dmul_rn(ra, ay)),
+                 pz = __dsub_rn(rz, __dmul_rn(ra, az));
+    const double pn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz)));
+    double mx = ax, my = ay, mz = az;
+    if (!(pn < core)) {
+        const double qx = __dsub_rn(__dmul_rn(ay, pz), __dmul_rn(az, py));
+        const double qy = __dsub_rn(__dmul_rn(az, px), __dmul_rn(ax, pz));
+        const double qz = __dsub_rn(__dmul_rn(ax, py), __dmul_rn(ay, px));
+        const double qn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)), __dmul_rn(qz, qz)));
+        mx = __ddiv_rn(qx, qn);
+        my = __ddiv_rn(qy, qn);
+        mz = __ddiv_rn(qz, qn);
+    }
+    m[c] = static_cast<T>(__dmul_rn(Ms, mx));
+    m[c + n] = static_cast<T>(__dmul_rn(Ms, my));
+    m[c + 2 * n] = static_cast<T>(__dmul_rn(Ms, mz));
+}
+
 template <class T>
 static void set_smem(const void* fn, int bytes, bool carve = true) {
     if (bytes > 48 * 1024)
@@ -620,6 +656,23 @@ void Engine<T>::set_uniform(const double dir[3]) {
     k_fill3<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
         M_[cur_], geo_.ncell, static_cast<T>(Ms * dir[0]), static_cast<T>(Ms * dir[1]), static_cast<T>(Ms * dir[2]));
     ck(cudaGetLastError(), "fill");
+    ck(cudaStreamSynchronize(stream_), "sync");
+}
+
+template <class T>
+void Engine<T>::set_vortex(int axis) {
+    static const double av[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+    if (axis < 0 || axis > 5) throw Error(MFD_EINVAL, "axisVector: bad axis");
+    const double* a = av[axis];
+    const bool along_x = a[0] != 0, along_y = a[1] != 0;
+    const int p1 = along_x ? grid_.ny : grid_.nx, p2 = (along_x || along_y) ? grid_.nz : grid_.ny;
+    if (p1 < 2 || p2 < 2)
+        throw Error(MFD_EINVAL, "makeVortexState: need >= 2 cells along each axis perpendicular to the core");
+    if (geo_.ncell > 0)
+        k_vortex<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
+            M_[cur_], grid_.nx, grid_.ny, geo_.nz, grid_.nz, geo_.k0, grid_.dx, grid_.dy, grid_.dz, a[0], a[1], a[2],
+            mat_.Ms);
+    ck(cudaGetLastError(), "vortex");
     ck(cudaStreamSynchronize(stream_), "sync");
 }
 

@@ -65,6 +65,9 @@ public:
     void set_uniform(const double dir[3]) override {
         for (auto& e : ranks_) e->set_uniform(dir);
     }
+    void set_vortex(int axis) override {
+        for (auto& e : ranks_) e->set_vortex(axis);
+    }
 
     void field(int which, double* x, double* y, double* z) override {
         if (which == 2 && !terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
