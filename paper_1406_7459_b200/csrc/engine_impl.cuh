@@ -175,8 +175,11 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             tw[k].x = static_cast<T>(cosl(a));
             tw[k].y = static_cast<T>(sinl(a));
         }
-        alloc(&tw_, TWN * sizeof(C2<T>));
-        ck(cudaMemcpy(tw_, tw.data(), TWN * sizeof(C2<T>), cudaMemcpyHostToDevice), "tw upload");
+        tw.resize(TW_ALLOC);
+        for (int LT = 1; LT <= TWN; LT *= 2)   // dense per-length copies (fft_engine.cuh)
+            for (int e = 0; e < LT; ++e) tw[TWN + LT + e] = tw[(long long)e * (TWN / LT)];
+        alloc(&tw_, TW_ALLOC * sizeof(C2<T>));
+        ck(cudaMemcpy(tw_, tw.data(), TW_ALLOC * sizeof(C2<T>), cudaMemcpyHostToDevice), "tw upload");
         k_ybuf<T><<<(Py_ + 127) / 128, 128, 0, stream_>>>(Py_, Py_, ybuf_);
         ck(cudaGetLastError(), "k_ybuf");
         // shared-memory opt-in for the instantiations this grid uses

@@ -86,11 +86,21 @@ __device__ __forceinline__ int natfreq(int p, int k) {
     else return (p / P::R1) + P::R0 * (p % P::R1) + P::R0 * P::R1 * k;
 }
 
-// Twiddle W_M^{e} (forward sign) from the global table of TWN entries.
+// Twiddle tables (one allocation): [0, TWN) W_TWN^e; then for every power of
+// two LT <= TWN a dense copy of the LT twiddles W_LT^e at [TWN + LT, TWN + 2 LT)
+// (same values: W_LT^e = W_TWN^(e TWN/LT)).  A transform of length L reads
+// only its dense L-entry table, so the lines it touches stay few and
+// L1-resident (the TWN-strided reads of a length-1024 transform touched every
+// line of the 32 KB table and mostly missed L1).
 constexpr int TWN = 4096;
-template <class T, int M>
+constexpr int TW_ALLOC = 3 * TWN;
+template <class T, int LT>
+__device__ __forceinline__ const C2<T>* tw_dense(const C2<T>* tw) { return tw + TWN + LT; }
+// W_M^e for a stage of a length-L transform (M divides L).
+template <class T, int L, int M>
 __device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) {
-    return __ldg(tw + e * (TWN / M));
+    static_assert(L % M == 0, "stage length must divide the transform length");
+    return __ldg(tw_dense<T, L>(tw) + e * (L / M));
 }
 
 // One stage over NCOL columns with NT threads.
@@ -104,7 +114,7 @@ __device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) 
 // ZIN (first forward stage only): inputs n1 >= R/2 are zero padding, not loaded.
 // HOUT (last inverse stage only): outputs n1 >= R/2 are outside the kept corner.
 template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, bool ZIN = false,
-          bool HOUT = false, bool NAT = false, class LD, class ST>
+          bool HOUT = false, bool NAT = false, int TWL = L, class LD, class ST>
 __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw) {
     using SI = StageInfo<T, L, s>;
     constexpr int R = SI::R, M = SI::M, MP = SI::MP;
@@ -144,12 +154,12 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
                 dft<T, R, false, ZIN>(v[i]);
                 if (MP > 1) {
 #pragma unroll
-                    for (int k = 1; k < R; ++k) v[i][k] = cmul<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
+                    for (int k = 1; k < R; ++k) v[i][k] = cmul<T>(v[i][k], tw_lookup<T, TWL, M>(tw, n2v[i] * k));
                 }
             } else {
                 if (MP > 1) {
 #pragma unroll
-                    for (int k = 1; k < R; ++k) v[i][k] = cmulc<T>(v[i][k], tw_lookup<T, M>(tw, n2v[i] * k));
+                    for (int k = 1; k < R; ++k) v[i][k] = cmulc<T>(v[i][k], tw_lookup<T, TWL, M>(tw, n2v[i] * k));
                 }
                 dft<T, R, true, false, HOUT>(v[i]);
             }
@@ -170,22 +180,22 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
 // every axis), so the first stage skips those loads and the first DIF level.
 // NAT: the last stage writes natural frequency order (instead of buffer order).
 template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
-          bool NAT = false, class LD0, class LDS, class STS, class STN>
+          bool NAT = false, int TWL = L, class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, PRUNE, false, NAT>(ld0, stn, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, PRUNE, false, NAT, TWL>(ld0, stn, tw);
     } else if constexpr (S == 2) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE, false, false, TWL>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT>(lds, stn, tw);
+        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT, TWL>(lds, stn, tw);
     } else if constexpr (S == 3) {
-        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE>(ld0, sts, tw);
+        fft_stage<T, L, 0, false, NCOL, NT, COLFAST, FIRST_SMEM, PRUNE, false, false, TWL>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, true>(lds, sts, tw);
+        fft_stage<T, L, 1, false, NCOL, NT, COLFAST, true, false, false, false, TWL>(lds, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 2, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT>(lds, stn, tw);
+        fft_stage<T, L, 2, false, NCOL, NT, COLFAST, LAST_SMEM, false, false, NAT, TWL>(lds, stn, tw);
     }
 }
 
@@ -195,22 +205,22 @@ __device__ __forceinline__ void fft_forward(LD0&& ld0, LDS&& lds, STS&& sts, STN
 // corner), so the last stage skips the other half.
 // NAT: the first stage reads natural frequency order (instead of buffer order).
 template <class T, int L, int NCOL, int NT, bool COLFAST, bool FIRST_SMEM, bool LAST_SMEM, bool PRUNE = true,
-          bool NAT = false, class LD0, class LDS, class STS, class STN>
+          bool NAT = false, int TWL = L, class LD0, class LDS, class STS, class STN>
 __device__ __forceinline__ void fft_inverse(LD0&& ld0, LDS&& lds, STS&& sts, STN&& stn,
                                             const C2<T>* __restrict__ tw) {
     constexpr int S = Plan<T, L>::S;
     if constexpr (S == 1) {
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, false, PRUNE, NAT>(ld0, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, FIRST_SMEM && LAST_SMEM, false, PRUNE, NAT, TWL>(ld0, stn, tw);
     } else if constexpr (S == 2) {
-        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT>(ld0, sts, tw);
+        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT, TWL>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE>(lds, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE, false, TWL>(lds, stn, tw);
     } else if constexpr (S == 3) {
-        fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT>(ld0, sts, tw);
+        fft_stage<T, L, 2, true, NCOL, NT, COLFAST, FIRST_SMEM, false, false, NAT, TWL>(ld0, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, true>(lds, sts, tw);
+        fft_stage<T, L, 1, true, NCOL, NT, COLFAST, true, false, false, false, TWL>(lds, sts, tw);
         __syncthreads();
-        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE>(lds, stn, tw);
+        fft_stage<T, L, 0, true, NCOL, NT, COLFAST, LAST_SMEM, false, PRUNE, false, TWL>(lds, stn, tw);
     }
 }
 
