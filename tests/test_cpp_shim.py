@@ -48,3 +48,20 @@ def test_driver_matches_oracle(prec):
     assert np.max(np.abs(m - ref.reduced_mean())) <= tol
     assert any(l.startswith("relax ") for l in lines)
     assert "invalid_argument Grid: cell counts must be >= 1" in out
+
+
+FMT_SRC = os.path.join(ROOT, "tests", "cpp", "formats_driver.cpp")
+
+
+def test_formats_shim_driver(tmp_path):
+    """include/magfd_b200/formats.hpp: config / dump / CSV / errors from plain g++ (host code, no GPU)."""
+    exe = str(tmp_path / "formats_driver")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), FMT_SRC, "-o", exe,
+                    "-L", PKG, "-lmagfd_b200", f"-Wl,-rpath,{PKG}"], check=True)
+    out = subprocess.run([exe, str(tmp_path)], check=True, capture_output=True, text=True).stdout
+    assert "defaults 22" in out      # 23 optional keys, init.kind given
+    assert "init.kind = vortex\n" in out and "grid.dx = 1.0000000000000001e-09\n" in out
+    assert "dump round trip bitwise" in out
+    assert "ConfigError config line 1: grid.nx must be >= 1, got 0" in out
+    assert "IoError cannot open for reading: " in out
+    assert (tmp_path / "t.csv").read_text().splitlines()[1] == "0,0,1,0,0,1,2,3,4,10,0.5"
