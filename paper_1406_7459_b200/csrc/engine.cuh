@@ -38,6 +38,9 @@ constexpr int kMaxL = 2048;
 // 512x512x64 f32 it is not faster than the plain K1 (0.33 vs 0.27 ms at 232
 // registers); kept selectable for further tuning.
 constexpr bool kUseK1Pipe = false;
+// Fuse the next step's x pass (K1) into K5 inside a graph chunk.
+constexpr bool kFuseK1 = true;
+constexpr long long kFuseK1MaxCells = 4LL << 20;
 // L2 prefetch (cp.async.bulk.prefetch) of the x passes' inputs one resident
 // wave of CTAs ahead, and of K5's epilogue rows while its FFT runs.
 // Bit mask (Geo::pfm): 1 K1 ahead, 2 K5 own M rows, 4 K5 spectrum ahead.
@@ -193,12 +196,13 @@ public:
 
 private:
     void build_tensor_from_octant();
-    void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr);
+    void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr, bool skip_k1 = false,
+                 bool fwd = false);
     // pass groups of one iteration: A = K1,K2 (slab -> send blocks), B = K3
     // (receive blocks, full z), C = K4,K5 (send blocks -> slab + LLG)
-    void enq_A(const Iter& it, int cur, cudaEvent_t* ev = nullptr);
+    void enq_A(const Iter& it, int cur, cudaEvent_t* ev = nullptr, bool skip_k1 = false);
     void enq_B(const Iter& it);
-    void enq_C(const Iter& it, int cur, cudaEvent_t* ev = nullptr);
+    void enq_C(const Iter& it, int cur, cudaEvent_t* ev = nullptr, bool fwd = false);
     void enq_local(const Iter& it, int cur);
     Ctl make_ctl(const Iter& it) const;
     StepIO make_io(const Iter& it) const;
@@ -250,6 +254,7 @@ private:
     bool small_x_ = false;                     // few rows: small-CTA variants of K1 / K5
     int k1_grid_ = 1, k1_smem_ = 0;
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
+    bool fuse_k1_ = false;                     // K5 also runs the next step's K1 (within a graph chunk)
     static constexpr int kMaxChunk = 256;
 
     std::map<std::pair<std::vector<Iter>, int>, cudaGraphExec_t> graphs_;

@@ -202,6 +202,8 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM, false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM, false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM, false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, true>, LCfg<T, L>::SMEM, false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, true>, LCfg<T, L>::SMEM, false);
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
             // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
             int nsm = 148;
@@ -244,6 +246,11 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         k5_blocks_ = (n + 255) / 256;
     }
     alloc(&partials_, (size_t)k5_blocks_ * 8 * sizeof(double));
+    // Measured on B200 (f32): fusing pays on small and mid grids, where K1 is a
+    // short latency-bound launch (SP4 0.023 -> 0.015 ms, 512x128x4 -8 %, 128^3 -6 %),
+    // and costs +1-3 % on the large films (K5's register budget then spills)
+    fuse_k1_ = kFuseK1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0 && geo_.ncell <= kFuseK1MaxCells;
+    if (const char* e = getenv("MFD_FUSE_K1")) fuse_k1_ = fuse_k1_ && atoi(e) != 0;   // A/B switch
     ck(cudaStreamSynchronize(stream_), "setup");
 }
 
@@ -388,10 +395,10 @@ void Engine<T>::enq_local(const Iter& it, int cur) {
 
 // A: K1 (x, R2C) + K2 (y forward) -> send blocks B_
 template <class T>
-void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev) {
+void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
     const Ctl ctl = make_ctl(it);
     const long long nrows = (long long)geo_.ny * geo_.nz;
-    with_pow2(geo_.N, [&]<int L>() {
+    if (!skip_k1) with_pow2(geo_.N, [&]<int L>() {
         using CF = XCfg<T, L>;
         if (k1_pipe_) {
             if constexpr (L >= 2)
@@ -445,7 +452,7 @@ void Engine<T>::enq_B(const Iter& it) {
 
 // C: K4 (y inverse, send blocks -> A) + K5 (x inverse + H_eff + LLG + Euler)
 template <class T>
-void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
+void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     const Ctl ctl = make_ctl(it);
     const StepIO io = make_io(it);
     const Halo<T> hl = halo_ptrs();
@@ -468,22 +475,17 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
         if constexpr (L >= 2 && L <= 256) {
             if (small_x_) {   // one row per CTA (few-row grids such as SP4)
                 using CS = LCfg<T, L, 1>;
-                if (io.sums)
-                    k_c2r_x_llg_v<T, L, true, 1><<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(
-                        geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
-                else
-                    k_c2r_x_llg_v<T, L, false, 1><<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(
-                        geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+                auto* k = io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 1, true> : k_c2r_x_llg_v<T, L, true, 1, false>)
+                                  : (fwd ? k_c2r_x_llg_v<T, L, false, 1, true> : k_c2r_x_llg_v<T, L, false, 1, false>);
+                k<<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
                 return;
             }
         }
-        if (geo_.nx % V16<T>::V == 0 && io.sums)
-            k_c2r_x_llg_v<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io,
-                                                                            ctl, hl);
-        else if (geo_.nx % V16<T>::V == 0)
-            k_c2r_x_llg_v<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_,
-                                                                             io, ctl, hl);
-        else
+        if (geo_.nx % V16<T>::V == 0) {
+            auto* k = io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 0, true> : k_c2r_x_llg_v<T, L, true, 0, false>)
+                              : (fwd ? k_c2r_x_llg_v<T, L, false, 0, true> : k_c2r_x_llg_v<T, L, false, 0, false>);
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+        } else
             k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl,
                                                                     hl);
     });
@@ -493,7 +495,7 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev) {
 // around K3 and the scalar allreduces are issued on the same stream, so they
 // are captured into the step graph with the kernels.
 template <class T>
-void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
+void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, bool skip_k1, bool fwd) {
     const size_t tsz = sizeof(T);
     if (events) ck(cudaEventRecord(ev[0], stream_), "event");
     if (tr_ && slab_.world > 1)
@@ -504,7 +506,7 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
         if (events)
             for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
     } else {
-        enq_A(it, cur, events ? ev : nullptr);
+        enq_A(it, cur, events ? ev : nullptr, skip_k1);
         if (events) ck(cudaEventRecord(ev[2], stream_), "event");
         if (stop_after_ == 1 || stop_after_ == 2) return;
         if (tr_ && slab_.world > 1) tr_->alltoall(B_, Br_, geo_.S_blk * sizeof(C2<T>), stream_);
@@ -512,7 +514,7 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev) {
         if (events) ck(cudaEventRecord(ev[3], stream_), "event");
         if (stop_after_ == 3) return;
         if (tr_ && slab_.world > 1) tr_->alltoall(Br_, B_, geo_.S_blk * sizeof(C2<T>), stream_);
-        enq_C(it, cur, events ? ev : nullptr);
+        enq_C(it, cur, events ? ev : nullptr, fwd);
         if (events) ck(cudaEventRecord(ev[5], stream_), "event");
         if (stop_after_ == 4) return;
     }
@@ -537,8 +539,14 @@ void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
         ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
         cudaMemsetAsync(torque_, 0, its.size() * sizeof(unsigned long long), stream_);
         int c = cur;
-        for (const Iter& it : its) {
-            enqueue(it, c);
+        bool fused_prev = false;
+        for (size_t j = 0; j < its.size(); ++j) {
+            const Iter& it = its[j];
+            // K5 of an updating iteration followed by another one in this graph
+            // also produces the next iteration's K1 output
+            const bool fuse = fuse_k1_ && it.update && j + 1 < its.size();
+            enqueue(it, c, false, nullptr, fused_prev, fuse);
+            fused_prev = fuse;
             if (it.update) c ^= 1;
         }
         ck(cudaStreamEndCapture(stream_, &g), "end capture");

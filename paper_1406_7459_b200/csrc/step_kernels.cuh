@@ -121,6 +121,21 @@ __device__ __forceinline__ bool halted(const Ctl& c) {
     return false;
 }
 
+// Real-to-complex post-process of one pair (k, N-k) of a row whose N-point
+// complex FFT of (x[2n], x[2n+1]) sits in scol (natural order):
+// X[k] = E + W^k O, X[N-k] = conj(E - W^k O), E/O the even/odd spectra.
+template <class T, int N>
+__device__ __forceinline__ void r2c_post(const C2<T>* scol, C2<T>* dst, int k, C2<T> w) {
+    const C2<T> zk = scol[xpad<T>(k & (N - 1))];
+    const C2<T> zn = cconj<T>(scol[xpad<T>((N - k) & (N - 1))]);
+    const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
+    const C2<T> d = csub<T>(zk, zn);
+    const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
+    const C2<T> wo = cmul<T>(w, O);
+    dst[k] = cadd<T>(E, wo);
+    if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
+}
+
 // ------------------------------------------------------------------ K1
 template <class T, int N, int RS = 0>
 __global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
@@ -1030,11 +1045,14 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // neighbours, so the stencil runs one component at a time (register use
 // independent of the component count); per cell and component the sum is
 // accumulated in the reference order x-, x+, y-, y+, z-, z+ (fields.hpp:33-48).
+// fsm (fused next-step x pass): the new M of the V cells also goes to shared
+// memory as (x[2n], x[2n+1]) pairs at component stride fstride.
 template <class T, bool SUMS>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                           const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
                                           const Halo<T>& hl, long long c0, int i0, int j, int k,
-                                          const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad) {
+                                          const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
+                                          C2<T>* fsm = nullptr, int fstride = 0) {
     constexpr int V = V16<T>::V;
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
     const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
@@ -1147,12 +1165,22 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         if (!all) bad = 1;
 #pragma unroll
         for (int c = 0; c < 3; ++c) vstore<T>(Mn + c * n + c0, mo[c]);
+        if (fsm) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < V; q += 2) fsm[c * fstride + xpad<T>((i0 + q) >> 1)] = mk<T>(mo[c][q], mo[c][q + 1]);
+        }
     }
 }
 
-template <class T, int N, bool SUMS, int RS = 0>
+// FWD: also run the NEXT step's x pass (K1) on the new M of this CTA's rows
+// while they are in shared memory, writing A in place of the spectrum this
+// CTA consumed (only its own rows: no cross-CTA hazard).  Saves K1's M read
+// and launch on every step but the first of a graph chunk.
+template <class T, int N, bool SUMS, int RS = 0, bool FWD = false>
 __global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
-k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
+k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
               T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
               Halo<T> hl) {
     using CF = LCfg<T, N, RS>;
@@ -1256,7 +1284,27 @@ k_c2r_x_llg_v(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __
                 hd[c][q] = z.x * scale;
                 hd[c][q + 1] = z.y * scale;
             }
-        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad);
+        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
+                           FWD ? sm + r * LP : nullptr, ROWS * LP);
+    }
+    if constexpr (FWD && N >= 2) {
+        // next step's K1 on the rows in shared memory (pairs beyond nx/2 are padding)
+        __syncthreads();
+        const int nxh = nx / 2;
+        auto ldf = [&](int col, int pos) -> C2<T> { return pos < nxh ? sm[col * LP + xpad<T>(pos)] : mk<T>(0, 0); };
+        auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
+        auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
+        fft_forward<T, N, NCOL, NT, false, true, true, true, true>(ldf, lds, sts, sts, tw);
+        __syncthreads();
+        constexpr int HPF = N / 2;
+        for (int e = threadIdx.x; e < NCOL * HPF; e += NT) {
+            const int col = e / HPF, kk = e % HPF;
+            const int comp = col / ROWS, r = col % ROWS;
+            if (row0 + r >= nrows) continue;
+            C2<T>* dst = A + ((long long)comp * nrows + row0 + r) * g.Hp;
+            r2c_post<T, N>(sm + col * LP, dst, kk, __ldg(tw_dense<T, 2 * N>(tw) + kk));
+            if (kk == 0) r2c_post<T, N>(sm + col * LP, dst, N / 2, __ldg(tw_dense<T, 2 * N>(tw) + N / 2));
+        }
     }
     block_finish<NT>(io, ctl, tmax, acc, bad);
 }
