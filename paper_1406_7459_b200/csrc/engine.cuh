@@ -40,6 +40,8 @@ constexpr int kMaxL = 2048;
 constexpr bool kUseK1Pipe = false;
 // Fuse the next step's x pass (K1) into K5 inside a graph chunk.
 constexpr bool kFuseK1 = true;
+// One-kernel K2-K4 for thin / small grids (YZCfg::OK).
+constexpr bool kYZSmall = true;
 constexpr long long kFuseK1MaxCells = 4LL << 20;
 // L2 prefetch (cp.async.bulk.prefetch) of the x passes' inputs one resident
 // wave of CTAs ahead, and of K5's epilogue rows while its FFT runs.
@@ -255,6 +257,17 @@ private:
     int k1_grid_ = 1, k1_smem_ = 0;
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     bool fuse_k1_ = false;                     // K5 also runs the next step's K1 (within a graph chunk)
+    bool yz_small_ = false;                    // K2-K4 as one kernel (k_fft_yz_small)
+    bool yz() const { return yz_small_ && stop_after_ == 0; }   // debug_stage needs the separate passes
+    // f.template operator()<Py, Pz>() when the single-kernel y-z pass exists for this grid
+    template <class F>
+    void with_yz(F&& f) const {
+        with_pow2(Py_, [&]<int LY>() {
+            with_pow2(Pz_, [&]<int LZ>() {
+                if constexpr (LZ <= 16 && YZCfg<T, LY, LZ>::OK) f.template operator()<LY, LZ>();
+            });
+        });
+    }
     static constexpr int kMaxChunk = 256;
 
     std::map<std::pair<std::vector<Iter>, int>, cudaGraphExec_t> graphs_;

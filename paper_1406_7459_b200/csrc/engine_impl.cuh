@@ -246,6 +246,12 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         k5_blocks_ = (n + 255) / 256;
     }
     alloc(&partials_, (size_t)k5_blocks_ * 8 * sizeof(double));
+    if (kYZSmall && terms_.demag && slab_.world == 1)
+        with_yz([&]<int LY, int LZ>() {
+            yz_small_ = true;
+            set_smem<T>((const void*)k_fft_yz_small<T, LY, LZ>, YZCfg<T, LY, LZ>::SMEM);
+        });
+    if (const char* e = getenv("MFD_YZ_SMALL")) yz_small_ = yz_small_ && atoi(e) != 0;   // A/B switch
     // Measured on B200 (f32): fusing pays on small and mid grids, where K1 is a
     // short latency-bound launch (SP4 0.023 -> 0.015 ms, 512x128x4 -8 %, 128^3 -6 %),
     // and costs +1-3 % on the large films (K5's register budget then spills)
@@ -416,6 +422,14 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
     });
     if (ev) ck(cudaEventRecord(ev[1], stream_), "event");
     if (stop_after_ == 1) return;
+    if (yz()) {   // K2 + K3 + K4 in one kernel (thin / small grids)
+        with_yz([&]<int LY, int LZ>() {
+            using CF = YZCfg<T, LY, LZ>;
+            k_fft_yz_small<T, LY, LZ><<<(geo_.Hx + CF::W - 1) / CF::W, CF::NT, CF::SMEM, stream_>>>(
+                geo_, A_, Kt_, tw_, ybuf_, ctl);
+        });
+        return;
+    }
     with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
@@ -430,7 +444,7 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
 template <class T>
 void Engine<T>::enq_B(const Iter& it) {
     const Ctl ctl = make_ctl(it);
-    if (geo_.Hv <= 0) return;
+    if (geo_.Hv <= 0 || yz()) return;
     with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
             dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
@@ -459,7 +473,7 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     const long long nrows = (long long)geo_.ny * geo_.nz;
     const T* Mc = M_[cur];
     T* Mn = M_[cur ^ 1];
-    with_pow2(Py_, [&]<int L>() {
+    if (!yz()) with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         if (2 * geo_.ny == L)

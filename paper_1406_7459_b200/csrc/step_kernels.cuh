@@ -666,6 +666,85 @@ k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int*
             if (k < nz && 2 * k < L) base[c * cstride + zoff(g, k)] = x[c][k];
 }
 
+// ------------------------------------------------------------ K2+K3+K4
+// Thin / small problems (Pz <= 16 and the y-z spectrum of a few x bins fits
+// in shared memory, e.g. SP4 128x32x1 and 512x128x4): one kernel per step does
+// the forward y FFT (A -> shared), the z transform + tensor product + inverse z
+// in registers (one thread per (y frequency, x bin), as k_fft_z_conv1) and
+// the inverse y FFT (shared -> A), so the three passes cost one launch and no
+// B round trip.  Arithmetic per column is the same as K2 / K3 / K4.
+template <class T, int LY, int LZ> struct YZCfg {
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr int NZH = LZ / 2 > 0 ? LZ / 2 : 1;               // z planes held (nz <= LZ/2)
+    static constexpr int W = cmax(1, cmin(4, 4096 / (3 * NZH * LY)));  // x bins per CTA
+    static constexpr int NCOL = 3 * NZH * W;                            // columns (comp, z, bin)
+    static constexpr int NT = 128;
+    static constexpr int SMEM = NCOL * LY * CS;
+    // Measured (f32): SP4 128x32x1 0.0164 -> 0.0107 ms/step; at 512x128x4 (W = 1)
+    // the per-CTA work is too thin and the separate passes win (0.040 vs 0.057 ms)
+    static constexpr bool OK = LZ <= 16 && Plan<T, LZ>::S <= 1 && SMEM <= 48 * 1024 && Plan<T, LY>::S >= 1 &&
+                               3 * NZH * LY <= 1024;
+};
+
+template <class T, int LY, int LZ>
+__global__ void __launch_bounds__(YZCfg<T, LY, LZ>::NT)
+k_fft_yz_small(Geo g, C2<T>* __restrict__ A, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
+               const int* __restrict__ ybuf, Ctl ctl) {
+    using CF = YZCfg<T, LY, LZ>;
+    constexpr int W = CF::W, NZH = CF::NZH, NCOL = CF::NCOL, NT = CF::NT;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);    // [y position][NCOL]
+    const int u0 = blockIdx.x * W;
+    const int ny = g.ny, nz = g.nz, Hp = g.Hp;
+    // column col = (comp * NZH + z) * W + w
+    auto arow = [&](int col, int y) -> long long {
+        const int w = col % W, z = (col / W) % NZH, c = col / (W * NZH);
+        return ((long long)(c * nz + z) * ny + y) * Hp + u0 + w;
+    };
+    auto zok = [&](int col) { return (col / W) % NZH < nz; };
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        return (pos < ny && zok(col)) ? A[arow(col, pos)] : mk<T>(0, 0);
+    };
+    auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * NCOL + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { sm[pos * NCOL + col] = v; };
+    fft_forward<T, LY, NCOL, NT, true, false, true>(ld0, lds, sts, sts, tw);
+    __syncthreads();
+    // z: one item per (y frequency v, bin w); frequencies in natural order
+    const int Hz = LZ / 2 + 1;
+    for (int e = threadIdx.x; e < LY * W; e += NT) {
+        const int w = e % W, v = e / W;
+        const int pos = ybuf[v];
+        const bool vhi = 2 * v > LY;
+        C2<T> x[3][LZ];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int k = 0; k < LZ; ++k)
+                x[c][k] = (k < NZH && 2 * k < LZ && k < nz) ? sm[pos * NCOL + (c * NZH + k) * W + w] : mk<T>(0, 0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dft<T, LZ, false, true>(x[c]);
+        const T* kb = Kt + ((long long)(vhi ? LY - v : v) * Hz * g.Wb + u0 + w) * 6;
+        const T sy = vhi ? T(-1) : T(1);
+#pragma unroll
+        for (int f = 0; f < LZ; ++f) {
+            const bool hi = 2 * f > LZ;
+            kmul<T>(x[0][f], x[1][f], x[2][f], kb + (long long)(hi ? LZ - f : f) * g.Wb * 6, sy, hi ? T(-1) : T(1));
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dft<T, LZ, true, false, true>(x[c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int k = 0; k < NZH; ++k) sm[pos * NCOL + (c * NZH + k) * W + w] = x[c][k];
+    }
+    __syncthreads();
+    auto stn = [&](int col, int pos, C2<T> v) {
+        if (pos < ny && zok(col)) A[arow(col, pos)] = v;
+    };
+    fft_inverse<T, LY, NCOL, NT, true, true, false>(lds, lds, sts, stn, tw);
+}
+
 // ------------------------------------------------------------------ K5
 // Local fields + LLG + Euler on one cell, in the reference's operation order
 // without FMA contraction (fields.hpp:33-48, 72-76, 246-250; dynamics.hpp:58-62, 101-108).
