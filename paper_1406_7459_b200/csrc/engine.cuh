@@ -42,6 +42,8 @@ constexpr bool kUseK1Pipe = false;
 constexpr bool kFuseK1 = true;
 // One-kernel K2-K4 for thin / small grids (YZCfg::OK).
 constexpr bool kYZSmall = true;
+// K2 input through TMA staging (persistent CTAs, next tile in flight).
+constexpr bool kK2Tma = true;
 constexpr long long kFuseK1MaxCells = 4LL << 20;
 // L2 prefetch (cp.async.bulk.prefetch) of the x passes' inputs one resident
 // wave of CTAs ahead, and of K5's epilogue rows while its FFT runs.
@@ -258,6 +260,9 @@ private:
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     bool fuse_k1_ = false;                     // K5 also runs the next step's K1 (within a graph chunk)
     bool yz_small_ = false;                    // K2-K4 as one kernel (k_fft_yz_small)
+    bool k2_tma_ = false;                      // K2 with TMA-staged input (k_fft_y_fwd_tma)
+    int k2_grid_ = 0, k2_box_ = 0;
+    CUtensorMap tmA_{};                        // A as [3 nz ny] x [Hp] 8-byte elements
     bool yz() const { return yz_small_ && stop_after_ == 0; }   // debug_stage needs the separate passes
     // f.template operator()<Py, Pz>() when the single-kernel y-z pass exists for this grid
     template <class F>

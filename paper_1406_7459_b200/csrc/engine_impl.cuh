@@ -252,6 +252,29 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             set_smem<T>((const void*)k_fft_yz_small<T, LY, LZ>, YZCfg<T, LY, LZ>::SMEM);
         });
     if (const char* e = getenv("MFD_YZ_SMALL")) yz_small_ = yz_small_ && atoi(e) != 0;   // A/B switch
+    if (kK2Tma && terms_.demag && !yz_small_ && (g.ny <= 256 || g.ny % 256 == 0)) {
+        with_pow2(Py_, [&]<int L>() {
+            if constexpr (YTCfg<T, L>::OK) {
+                const int cs = (int)sizeof(C2<T>);
+                k2_box_ = std::min(256, g.ny);
+                if (make_tmap_2d(&tmA_, A_, (unsigned long long)geo_.Hp * cs / 8,
+                                 3ULL * geo_.nz * geo_.ny, (unsigned long long)geo_.Hp * cs,
+                                 (unsigned)(YTCfg<T, L>::W * cs / 8), (unsigned)k2_box_)) {
+                    set_smem<T>((const void*)k_fft_y_fwd_tma<T, L, true>, YTCfg<T, L>::SMEM);
+                    set_smem<T>((const void*)k_fft_y_fwd_tma<T, L, false>, YTCfg<T, L>::SMEM);
+                    int per = 0, nsm = 148;
+                    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
+                    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fft_y_fwd_tma<T, L, true>,
+                                                                     YTCfg<T, L>::NT, YTCfg<T, L>::SMEM),
+                       "occupancy");
+                    const long long tiles = 3LL * geo_.nz * ((geo_.Hx + YTCfg<T, L>::W - 1) / YTCfg<T, L>::W);
+                    k2_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per) * nsm);
+                    k2_tma_ = per > 0;
+                }
+            }
+        });
+    }
+    if (const char* e = getenv("MFD_K2_TMA")) k2_tma_ = k2_tma_ && atoi(e) != 0;   // A/B switch
     // Measured on B200 (f32): fusing pays on small and mid grids, where K1 is a
     // short latency-bound launch (SP4 0.023 -> 0.015 ms, 512x128x4 -8 %, 128^3 -6 %),
     // and costs +1-3 % on the large films (K5's register budget then spills)
@@ -427,6 +450,17 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
             using CF = YZCfg<T, LY, LZ>;
             k_fft_yz_small<T, LY, LZ><<<(geo_.Hx + CF::W - 1) / CF::W, CF::NT, CF::SMEM, stream_>>>(
                 geo_, A_, Kt_, tw_, ybuf_, ctl);
+        });
+        return;
+    }
+    if (k2_tma_) {
+        with_pow2(Py_, [&]<int L>() {
+            if constexpr (YTCfg<T, L>::OK) {
+                using CF = YTCfg<T, L>;
+                const int ntx = (geo_.Hx + CF::W - 1) / CF::W;
+                auto* k = 2 * geo_.ny == L ? k_fft_y_fwd_tma<T, L, true> : k_fft_y_fwd_tma<T, L, false>;
+                k<<<k2_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmA_, B_, tw_, ctl, ntx, k2_box_);
+            }
         });
         return;
     }

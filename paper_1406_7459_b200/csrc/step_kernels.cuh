@@ -15,6 +15,7 @@
 //                                     interleaved per bin
 #pragma once
 #include "fft_engine.cuh"
+#include "tma.cuh"
 
 namespace mfd {
 
@@ -340,6 +341,76 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
     // twiddles from the TWN-strided copy: measured faster for this pass than the
     // dense L table (0.314 vs 0.342 ms, 512x512x64 f32), unlike every other pass
     fft_forward<T, L, W, NT, true, false, false, true, false, kK2StridedTw ? TWN : L>(ld0, lds, sts, stn, tw);
+}
+
+// K2 with TMA-staged input (two-stage plans): persistent CTAs; the A tile of
+// the next (x-bin block, plane, component) streams into a shared staging
+// buffer (cp.async.bulk.tensor, mbarrier-completed) while the current tile runs
+// its second FFT stage, so no warp waits on global loads.  Same arithmetic as
+// k_fft_y_fwd.
+template <class T, int L> struct YTCfg {
+    static constexpr int W = YCfg<T, L>::W, NT = YCfg<T, L>::NT, CS = sizeof(C2<T>);
+    static constexpr int SMEM = W * L * CS + W * (L / 2) * CS + 128;   // work + staging (ny <= L/2 rows) + align
+    // Measured (f32): Py = 1024 0.317 -> 0.243 ms (512x512x64); at Py = 256 the
+    // plain kernel is ~10 % faster (short tiles), so staging starts at 512
+    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 110 * 1024 && L >= 512;
+};
+
+template <class T, int L, bool FY>
+__global__ void __launch_bounds__(YTCfg<T, L>::NT, 2)
+k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restrict__ B,
+                const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int box_rows) {
+    using CF = YTCfg<T, L>;
+    constexpr int W = CF::W, NT = CF::NT;
+    constexpr int TWL = kK2StridedTw ? TWN : L;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* work = reinterpret_cast<C2<T>*>(smem_raw);
+    // TMA destinations must be 128-byte aligned
+    C2<T>* stage = reinterpret_cast<C2<T>*>((reinterpret_cast<uintptr_t>(work + W * L) + 127) & ~uintptr_t(127));
+    __shared__ uint64_t bar;
+    const int ny = g.ny, nz = g.nz, Wb = g.Wb;
+    const int ntiles = ntx * nz * 3;
+    int t = blockIdx.x;
+    if (t >= ntiles) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+    }
+    __syncthreads();
+    auto issue = [&](int tt) {   // one thread
+        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
+        const int row0 = (comp * nz + k) * ny;
+        mbar_arrive_expect_tx(&bar, (unsigned)(ny * W * CF::CS));
+        for (int r = 0; r < ny; r += box_rows)
+            tma_load_2d(stage + r * W, &tmA, bx * W * (CF::CS / 8), row0 + r, &bar);
+    };
+    if (threadIdx.x == 0) issue(t);
+    unsigned parity = 0;
+    auto lds = [&](int col, int pos) -> C2<T> { return work[yswz<T, L, W>(pos) * W + col]; };
+    auto sts = [&](int col, int pos, C2<T> v) { work[yswz<T, L, W>(pos) * W + col] = v; };
+    auto ld0 = [&](int col, int pos) -> C2<T> {
+        if (!FY && pos >= ny) return mk<T>(0, 0);
+        return stage[pos * W + col];
+    };
+#pragma unroll 1
+    for (; t < ntiles; t += gridDim.x) {
+        const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
+        const int u0 = bx * W;
+        C2<T>* dst = B + (u0 / Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % Wb;
+        auto stn = [&](int col, int pos, C2<T> v) { dst[pos * Wb + col] = v; };
+        mbar_wait(&bar, parity);
+        parity ^= 1;
+        fft_stage<T, L, 0, false, W, NT, true, false, true, false, false, TWL>(ld0, sts, tw);
+        __syncthreads();   // staging consumed, stage-0 output visible
+        if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+            fence_proxy_async_smem();
+            issue(t + gridDim.x);
+        }
+        fft_stage<T, L, 1, false, W, NT, true, false, false, false, false, TWL>(lds, stn, tw);
+        __syncthreads();   // work buffer free for the next tile
+    }
 }
 
 // ------------------------------------------------------------------ K4
