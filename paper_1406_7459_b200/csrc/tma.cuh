@@ -49,6 +49,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// 3-D tensor tile global -> shared
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -57,5 +65,8 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 // 8-byte elements with a row pitch of `pitch` elements; box = box_cols x box_rows.
 bool make_tmap_2d(CUtensorMap* map, const void* base, unsigned long long cols, unsigned long long rows,
                   unsigned long long pitch_bytes, unsigned box_cols, unsigned box_rows);
+// 3-D: dims d0 (contiguous, 8-byte elements), d1, d2; byte strides of d1, d2; box b0 x b1 x b2.
+bool make_tmap_3d(CUtensorMap* map, const void* base, const unsigned long long dims[3],
+                  const unsigned long long strides_bytes[2], const unsigned box[3]);
 
 } // namespace mfd
