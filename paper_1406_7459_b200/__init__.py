@@ -23,7 +23,7 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmagfd_b200.so")
+LIB_PATH = os.environ.get("MFD_LIB") or os.path.join(HERE, "libmagfd_b200.so")   # MFD_LIB: A/B builds (tools/build_variant.sh)
 
 MU0 = 4.0e-7 * 3.14159265358979323846      # constants.hpp:9
 GAMMA_E = 1.760859630e11                    # constants.hpp:12

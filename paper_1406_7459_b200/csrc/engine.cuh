@@ -44,6 +44,8 @@ constexpr bool kFuseK1 = true;
 constexpr bool kYZSmall = true;
 // K2 input through TMA staging (persistent CTAs, next tile in flight).
 constexpr bool kK2Tma = true;
+// K4 input through a ring of TMA-staged half tiles (persistent CTAs).
+constexpr bool kK4Tma = true;
 constexpr long long kFuseK1MaxCells = 4LL << 20;
 // L2 prefetch (cp.async.bulk.prefetch) of the x passes' inputs one resident
 // wave of CTAs ahead, and of K5's epilogue rows while its FFT runs.
@@ -263,6 +265,9 @@ private:
     bool k2_tma_ = false;                      // K2 with TMA-staged input (k_fft_y_fwd_tma)
     int k2_grid_ = 0, k2_box_ = 0;
     CUtensorMap tmA_{};                        // A as [3 nz ny] x [Hp] 8-byte elements
+    bool k4_tma_ = false;                      // K4 with TMA-staged input (k_fft_y_inv_tma)
+    int k4_grid_ = 0;
+    CUtensorMap tmB_{};                        // B as [G 3 nz Py] x [Wb] 8-byte elements
     bool yz() const { return yz_small_ && stop_after_ == 0; }   // debug_stage needs the separate passes
     // f.template operator()<Py, Pz>() when the single-kernel y-z pass exists for this grid
     template <class F>

@@ -275,6 +275,29 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         });
     }
     if (const char* e = getenv("MFD_K2_TMA")) k2_tma_ = k2_tma_ && atoi(e) != 0;   // A/B switch
+    if (kK4Tma && terms_.demag && !yz_small_) {
+        with_pow2(Py_, [&]<int L>() {
+            if constexpr (YICfg<T, L>::OK) {
+                using CF = YICfg<T, L>;
+                const int cs = (int)sizeof(C2<T>);
+                if (make_tmap_2d(&tmB_, B_, (unsigned long long)geo_.Wb * cs / 8,
+                                 (unsigned long long)geo_.G * 3 * geo_.nz * Py_,
+                                 (unsigned long long)geo_.Wb * cs, (unsigned)(CF::W * cs / 8), (unsigned)CF::BOX)) {
+                    set_smem<T>((const void*)k_fft_y_inv_tma<T, L, true>, CF::SMEM);
+                    set_smem<T>((const void*)k_fft_y_inv_tma<T, L, false>, CF::SMEM);
+                    int per = 0, nsm = 148;
+                    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
+                    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fft_y_inv_tma<T, L, true>, CF::NT,
+                                                                     CF::SMEM),
+                       "occupancy");
+                    const long long tiles = 3LL * geo_.nz * ((geo_.Hx + CF::W - 1) / CF::W);
+                    k4_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per) * nsm);
+                    k4_tma_ = per > 0;
+                }
+            }
+        });
+    }
+    if (const char* e = getenv("MFD_K4_TMA")) k4_tma_ = k4_tma_ && atoi(e) != 0;   // A/B switch
     // Measured on B200 (f32): fusing pays on small and mid grids, where K1 is a
     // short latency-bound launch (SP4 0.023 -> 0.015 ms, 512x128x4 -8 %, 128^3 -6 %),
     // and costs +1-3 % on the large films (K5's register budget then spills)
@@ -507,7 +530,15 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     const long long nrows = (long long)geo_.ny * geo_.nz;
     const T* Mc = M_[cur];
     T* Mn = M_[cur ^ 1];
-    if (!yz()) with_pow2(Py_, [&]<int L>() {
+    if (!yz() && k4_tma_) with_pow2(Py_, [&]<int L>() {
+        if constexpr (YICfg<T, L>::OK) {
+            using CF = YICfg<T, L>;
+            const int ntx = (geo_.Hx + CF::W - 1) / CF::W;
+            auto* k = 2 * geo_.ny == L ? k_fft_y_inv_tma<T, L, true> : k_fft_y_inv_tma<T, L, false>;
+            k<<<k4_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, A_, tw_, ctl, ntx);
+        }
+    });
+    else if (!yz()) with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
         if (2 * geo_.ny == L)

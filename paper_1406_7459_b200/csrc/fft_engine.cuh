@@ -113,9 +113,11 @@ __device__ __forceinline__ C2<T> tw_lookup(const C2<T>* __restrict__ tw, int e) 
 // when source and destination are the same shared buffer.
 // ZIN (first forward stage only): inputs n1 >= R/2 are zero padding, not loaded.
 // HOUT (last inverse stage only): outputs n1 >= R/2 are outside the kept corner.
+struct NoHook { __device__ void operator()() const {} };
+// mid: called after the SYNC_MID barrier (every gather of the stage is done)
 template <class T, int L, int s, bool INV, int NCOL, int NT, bool COLFAST, bool SYNC_MID, bool ZIN = false,
-          bool HOUT = false, bool NAT = false, int TWL = L, class LD, class ST>
-__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw) {
+          bool HOUT = false, bool NAT = false, int TWL = L, class LD, class ST, class MID = NoHook>
+__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restrict__ tw, MID&& mid = MID{}) {
     using SI = StageInfo<T, L, s>;
     constexpr int R = SI::R, M = SI::M, MP = SI::MP;
     constexpr int TPC = L / R;
@@ -145,7 +147,10 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const C2<T>* __restr
                               : ld(col, (NATF && INV) ? natfreq<T, L>(p, j) : basev[i] + MP * j);
         }
     }
-    if (SYNC_MID) __syncthreads();
+    if (SYNC_MID) {
+        __syncthreads();
+        mid();
+    }
 #pragma unroll
     for (int i = 0; i < TPT; ++i) {
         const int q = threadIdx.x + i * NT;

@@ -436,6 +436,88 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
     fft_inverse<T, L, W, NT, true, false, false>(ld0, lds, sts, stn, tw);
 }
 
+// K4 with TMA-staged input (two-stage plans): persistent CTAs over a ring of
+// three half-tile slots.  Tile i (L rows x W bins of B) lands as two halves in
+// slots (2i) % 3 and (2i+1) % 3.  The transposed first inverse stage (stage 1,
+// MP = 1) reads and writes the L/R0 contiguous rows of its task in place, so it
+// needs no second buffer; once the last stage has gathered the tile into
+// registers both its slots are free and the next tile's second half and the
+// tile after that's first half are issued into them, so every load is in
+// flight for at least one stage of compute.  Same arithmetic as k_fft_y_inv.
+template <class T, int L> struct YICfg {
+    static constexpr int W = YCfg<T, L>::W, NT = YCfg<T, L>::NT, CS = sizeof(C2<T>);
+    static constexpr int HALF = L / 2;                        // rows per slot
+    static constexpr int SLOT = HALF * W * CS;
+    static constexpr int SMEM = 3 * SLOT + 128;               // + TMA alignment
+    static constexpr int BOX = HALF < 256 ? HALF : 256;       // TMA box rows (<= 256)
+    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 110 * 1024 && L >= 256 && W * CS >= 16;
+};
+
+template <class T, int L, bool FY>
+__global__ void __launch_bounds__(YICfg<T, L>::NT, 2)
+k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restrict__ A,
+                const C2<T>* __restrict__ tw, Ctl ctl, int ntx) {
+    using CF = YICfg<T, L>;
+    constexpr int W = CF::W, NT = CF::NT, HALF = CF::HALF;
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C2<T>* slot0 = reinterpret_cast<C2<T>*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    __shared__ uint64_t bar[3];
+    const int ny = g.ny, nz = g.nz, Hp = g.Hp, Wb = g.Wb;
+    const int ntiles = ntx * nz * 3;
+    if ((int)blockIdx.x >= ntiles) return;
+    // fill f = 2 i + h (tile i of this CTA, half h) -> slot f % 3, phase (f / 3) & 1
+    auto issue = [&](int i, int h) {   // one thread
+        const int tt = blockIdx.x + i * gridDim.x;
+        if (tt >= ntiles) return;
+        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
+        const int u0 = bx * W;
+        const long long row0 = (((long long)(u0 / Wb) * 3 + comp) * nz + k) * L + h * HALF;
+        const int s = (2 * i + h) % 3;
+        mbar_arrive_expect_tx(&bar[s], (unsigned)CF::SLOT);
+        for (int r = 0; r < HALF; r += CF::BOX)
+            tma_load_2d(slot0 + s * (HALF * W) + r * W, &tmB, (u0 % Wb) * (CF::CS / 8), (int)(row0 + r), &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 3; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmB);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { issue(0, 0); issue(0, 1); issue(1, 0); }
+#pragma unroll 1
+    for (int i = 0;; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) break;
+        const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
+        const int u0 = bx * W;
+        C2<T>* sa = slot0 + ((2 * i) % 3) * (HALF * W);
+        C2<T>* sb = slot0 + ((2 * i + 1) % 3) * (HALF * W);
+        auto at = [&](int col, int pos) -> C2<T>& { return (pos < HALF ? sa : sb)[(pos & (HALF - 1)) * W + col]; };
+        auto lds = [&](int col, int pos) -> C2<T> { return at(col, pos); };
+        auto sts = [&](int col, int pos, C2<T> v) { at(col, pos) = v; };
+        C2<T>* dst = A + ((long long)comp * nz + k) * ny * Hp + u0;
+        auto stn = [&](int col, int pos, C2<T> v) {
+            if (FY || pos < ny) dst[pos * Hp + col] = v;
+        };
+        mbar_wait(&bar[(2 * i) % 3], ((2 * i) / 3) & 1);
+        mbar_wait(&bar[(2 * i + 1) % 3], ((2 * i + 1) / 3) & 1);
+        // transposed stage 1: in place, per task (no barrier between gather and scatter)
+        fft_stage<T, L, 1, true, W, NT, true, false>(lds, sts, tw);
+        __syncthreads();
+        // transposed stage 0: gather (all rows), barrier, then refill both slots
+        // while this tile's DFTs and HBM stores run
+        fft_stage<T, L, 0, true, W, NT, true, true, false, true, false, L>(
+            lds, stn, tw, [&] {
+                if (threadIdx.x == 0) {
+                    fence_proxy_async_smem();
+                    issue(i + 1, 1);
+                    issue(i + 2, 0);
+                }
+            });
+    }
+}
+
 // ------------------------------------------------------------------ K3
 // One CTA: W x-bins, the y-frequency pair {v, Py-v}, all three components,
 // full z columns.  Forward z (nz active inputs) -> per-bin symmetric real
@@ -554,14 +636,22 @@ __device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* _
 template <class T, int L> struct Z2Cfg {
     static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
     static constexpr int CS = sizeof(C2<T>);
+#ifdef MFD_K3W
+    static constexpr int W = MFD_K3W;
+#else
     static constexpr int W = (sizeof(T) == 4 ? 16 : 8) / (R1 >= 16 ? 2 : 1);
+#endif
     static constexpr int NCOL = 6 * W;
     static constexpr int NT = W * R1 * 2;
     static constexpr int SMEM = NCOL * L * CS;
     // resident CTAs per SM the register budget is sized for (shared memory permitting)
     // tensor bins loaded one phase ahead (register budget: R1 <= 8 only)
     static constexpr bool KPRE = R1 <= 8;
+#ifdef MFD_K3MINB
+    static constexpr int MINB = MFD_K3MINB;
+#else
     static constexpr int MINB = KPRE ? cmax(1, cmin(2, (200 * 1024) / SMEM)) : 1;
+#endif
 };
 
 // FZ: nz == Pz/2, so the pruned first/last stages never meet a plane >= nz.
