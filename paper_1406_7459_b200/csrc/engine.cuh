@@ -207,7 +207,7 @@ private:
     // pass groups of one iteration: A = K1,K2 (slab -> send blocks), B = K3
     // (receive blocks, full z), C = K4,K5 (send blocks -> slab + LLG)
     void enq_A(const Iter& it, int cur, cudaEvent_t* ev = nullptr, bool skip_k1 = false);
-    void enq_B(const Iter& it);
+    void enq_B(const Iter& it, cudaEvent_t* ev = nullptr);
     void enq_C(const Iter& it, int cur, cudaEvent_t* ev = nullptr, bool fwd = false);
     void enq_local(const Iter& it, int cur);
     Ctl make_ctl(const Iter& it) const;
@@ -241,7 +241,7 @@ private:
     T* halo_ = nullptr;                  // [2][3][ny][nx]: lo, hi planes (world > 1)
     C2<T>* A_ = nullptr;
     C2<T>* B_ = nullptr;                 // send-side blocks (== receive side on one GPU)
-    C2<T>* Br_ = nullptr;                // receive-side blocks (world > 1)
+    C2<T>* Ar_ = nullptr;                // receive-side A blocks (world > 1; = A_ on one GPU)
     T* Kt_ = nullptr;
     C2<T>* tw_ = nullptr;
     int* ybuf_ = nullptr;

@@ -2,6 +2,7 @@
 // engine_f64.cu (explicit instantiation keeps the two builds parallel).
 #pragma once
 #include <algorithm>
+#include <cstdio>
 
 #include "engine.cuh"
 
@@ -99,18 +100,20 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     geo_.Px = Px; geo_.Py = Py_; geo_.Pz = Pz_;
     geo_.N = Px / 2;
     geo_.Hx = geo_.N + 1;
-    geo_.Hp = (geo_.Hx + 15) / 16 * 16;
+    // A row pitch: all bins on one GPU; the x-bin block width when sharded
     geo_.ncell = (long long)g.nx * g.ny * nzl;
     geo_.nzg = g.nz;
     geo_.k0 = slab_.k0;
     geo_.G = G;
     geo_.ublk = slab_.rank;
     // x-bin blocks: multiples of 16 so no y/z tile straddles two ranks
-    geo_.Wb = G == 1 ? geo_.Hp : ((geo_.Hx + G - 1) / G + 15) / 16 * 16;
+    geo_.Wb = G == 1 ? (geo_.Hx + 15) / 16 * 16 : ((geo_.Hx + G - 1) / G + 15) / 16 * 16;
+    geo_.Hp = geo_.Wb;
+    geo_.binv = (unsigned)(((1u << 24) + geo_.Wb - 1) / geo_.Wb);
     geo_.Hv = std::max(0, std::min(geo_.Wb, geo_.Hx - slab_.rank * geo_.Wb));
+    geo_.SA = 3LL * nzl * g.ny * geo_.Hp;
     geo_.S_k = (long long)Py_ * geo_.Wb;
-    geo_.S_c = (long long)nzl * geo_.S_k;
-    geo_.S_blk = 3 * geo_.S_c;
+    geo_.S_c = (long long)g.nz * geo_.S_k;   // B holds all nzg planes of this rank's x-bin block
     ncell = geo_.ncell;
     Hy_ = Py_ / 2 + 1;
     Hz_ = Pz_ / 2 + 1;
@@ -162,10 +165,11 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     if (G > 1) alloc(&halo_, 2 * 3 * (long long)g.nx * g.ny * sizeof(T));
     if (terms_.demag) {
         const long long nrows = (long long)g.ny * nzl;
-        alloc(&A_, 3 * nrows * geo_.Hp * sizeof(C2<T>));
-        alloc(&B_, (size_t)G * geo_.S_blk * sizeof(C2<T>));
-        if (G > 1) alloc(&Br_, (size_t)G * geo_.S_blk * sizeof(C2<T>));
-        else Br_ = B_;
+        (void)nrows;
+        alloc(&A_, (size_t)G * geo_.SA * sizeof(C2<T>));          // send blocks (G = 1: the A spectrum)
+        if (G > 1) alloc(&Ar_, (size_t)G * geo_.SA * sizeof(C2<T>));   // receive blocks
+        else Ar_ = A_;
+        alloc(&B_, (size_t)3 * geo_.S_c * sizeof(C2<T>));
         alloc(&Kt_, 6 * (long long)Hy_ * Hz_ * geo_.Wb * sizeof(T));
         alloc(&ybuf_, Py_ * sizeof(int));   // buffer row of every y frequency
         // twiddles exp(-2 pi i k / TWN), long double on the host, cast to T (fft.hpp:70-74)
@@ -185,8 +189,9 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         // shared-memory opt-in for the instantiations this grid uses
         with_pow2(geo_.N, [&]<int L>() {
             set_smem<T>((const void*)k_r2c_x<T, L>, XCfg<T, L>::SMEM);
+            if (G > 1) set_smem<T>((const void*)k_r2c_x<T, L, 0, true>, XCfg<T, L>::SMEM);
             // pipelined K1: persistent grid sized by occupancy
-            k1_pipe_ = kUseK1Pipe && L >= 2 && g.nx % 2 == 0 && (geo_.ncell * (long long)sizeof(T)) % 16 == 0;
+            k1_pipe_ = kUseK1Pipe && G == 1 && L >= 2 && g.nx % 2 == 0 && (geo_.ncell * (long long)sizeof(T)) % 16 == 0;
             if constexpr (L >= 2) if (k1_pipe_) {
                 const int sm_bytes = XCfg<T, L>::SMEM + 2 * XCfg<T, L>::ROWS * L * (int)sizeof(T);
                 set_smem<T>((const void*)k_r2c_x_pipe<T, L>, sm_bytes);
@@ -204,6 +209,11 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM, false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, true>, LCfg<T, L>::SMEM, false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, true>, LCfg<T, L>::SMEM, false);
+            if (G > 1) {
+                set_smem<T>((const void*)k_c2r_x_llg<T, L, true>, LCfg<T, L>::SMEM, false);
+                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, false, true>, LCfg<T, L>::SMEM, false);
+                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, false, true>, LCfg<T, L>::SMEM, false);
+            }
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
             // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
             int nsm = 148;
@@ -229,10 +239,8 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
         });
         with_pow2(Pz_, [&]<int L>() {
             if constexpr (z_variant<T, L>() == 2) {
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, true, false>, Z2Cfg<T, L>::SMEM);
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, false, false>, Z2Cfg<T, L>::SMEM);
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, true, true>, Z2Cfg<T, L>::SMEM);
-                set_smem<T>((const void*)k_fft_z_conv2<T, L, false, true>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, true>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, false>, Z2Cfg<T, L>::SMEM);
             }
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
@@ -257,8 +265,8 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             if constexpr (YTCfg<T, L>::OK) {
                 const int cs = (int)sizeof(C2<T>);
                 k2_box_ = std::min(256, g.ny);
-                if (make_tmap_2d(&tmA_, A_, (unsigned long long)geo_.Hp * cs / 8,
-                                 3ULL * geo_.nz * geo_.ny, (unsigned long long)geo_.Hp * cs,
+                if (make_tmap_2d(&tmA_, Ar_, (unsigned long long)geo_.Hp * cs / 8,
+                                 (unsigned long long)geo_.G * 3 * geo_.nz * geo_.ny, (unsigned long long)geo_.Hp * cs,
                                  (unsigned)(YTCfg<T, L>::W * cs / 8), (unsigned)k2_box_)) {
                     set_smem<T>((const void*)k_fft_y_fwd_tma<T, L, true>, YTCfg<T, L>::SMEM);
                     set_smem<T>((const void*)k_fft_y_fwd_tma<T, L, false>, YTCfg<T, L>::SMEM);
@@ -267,7 +275,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
                     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fft_y_fwd_tma<T, L, true>,
                                                                      YTCfg<T, L>::NT, YTCfg<T, L>::SMEM),
                        "occupancy");
-                    const long long tiles = 3LL * geo_.nz * ((geo_.Hx + YTCfg<T, L>::W - 1) / YTCfg<T, L>::W);
+                    const long long tiles = 3LL * geo_.nzg * ((geo_.Hv + YTCfg<T, L>::W - 1) / YTCfg<T, L>::W);
                     k2_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per) * nsm);
                     k2_tma_ = per > 0;
                 }
@@ -281,7 +289,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
                 using CF = YICfg<T, L>;
                 const int cs = (int)sizeof(C2<T>);
                 if (make_tmap_2d(&tmB_, B_, (unsigned long long)geo_.Wb * cs / 8,
-                                 (unsigned long long)geo_.G * 3 * geo_.nz * Py_,
+                                 3ULL * geo_.nzg * Py_,
                                  (unsigned long long)geo_.Wb * cs, (unsigned)(CF::W * cs / 8), (unsigned)CF::BOX)) {
                     set_smem<T>((const void*)k_fft_y_inv_tma<T, L, true>, CF::SMEM);
                     set_smem<T>((const void*)k_fft_y_inv_tma<T, L, false>, CF::SMEM);
@@ -290,7 +298,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
                     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fft_y_inv_tma<T, L, true>, CF::NT,
                                                                      CF::SMEM),
                        "occupancy");
-                    const long long tiles = 3LL * geo_.nz * ((geo_.Hx + CF::W - 1) / CF::W);
+                    const long long tiles = 3LL * geo_.nzg * ((geo_.Hv + CF::W - 1) / CF::W);
                     k4_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per) * nsm);
                     k4_tma_ = per > 0;
                 }
@@ -301,8 +309,13 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     // Measured on B200 (f32): fusing pays on small and mid grids, where K1 is a
     // short latency-bound launch (SP4 0.023 -> 0.015 ms, 512x128x4 -8 %, 128^3 -6 %),
     // and costs +1-3 % on the large films (K5's register budget then spills)
-    fuse_k1_ = kFuseK1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0 && geo_.ncell <= kFuseK1MaxCells;
-    if (const char* e = getenv("MFD_FUSE_K1")) fuse_k1_ = fuse_k1_ && atoi(e) != 0;   // A/B switch
+    fuse_k1_ = kFuseK1 && G == 1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0 && geo_.ncell <= kFuseK1MaxCells;
+    if (const char* e = getenv("MFD_FUSE_K1"))   // A/B switch: 0 off, 2 on regardless of the grid size
+        fuse_k1_ = atoi(e) == 2 ? (kFuseK1 && G == 1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0)
+                                : fuse_k1_ && atoi(e) != 0;
+    if (getenv("MFD_VERBOSE"))
+        fprintf(stderr, "mfd: K2 tma %d grid %d | K4 tma %d grid %d | yz_small %d fuse_k1 %d\n", (int)k2_tma_,
+                k2_grid_, (int)k4_tma_, k4_grid_, (int)yz_small_, (int)fuse_k1_);
     ck(cudaStreamSynchronize(stream_), "setup");
 }
 
@@ -313,7 +326,7 @@ Engine<T>::~Engine() {
     void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, oct_, err_, torque_, sums_, partials_, ticket_, halo_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    if (Br_ && Br_ != B_) cudaFree(Br_);
+    if (Ar_ && Ar_ != A_) cudaFree(Ar_);
     delete tr_;
     if (h_torque_) cudaFreeHost(h_torque_);
     if (h_sums_) cudaFreeHost(h_sums_);
@@ -445,7 +458,7 @@ void Engine<T>::enq_local(const Iter& it, int cur) {
         geo_, M_[cur], M_[cur ^ 1], H_, lp_, make_io(it), make_ctl(it), halo_ptrs());
 }
 
-// A: K1 (x, R2C) + K2 (y forward) -> send blocks B_
+// A: K1 (x, R2C) -> A_ (on several GPUs: the send blocks, one per rank's x-bins)
 template <class T>
 void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
     const Ctl ctl = make_ctl(it);
@@ -459,69 +472,92 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
             if constexpr (L >= 2 && L <= 256) {
                 using CS = XCfg<T, L, 2>;
                 dim3 grid((unsigned)((nrows + 1) / 2), 3);
-                k_r2c_x<T, L, 2><<<grid, CS::NT, CS::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+                auto* k = geo_.G > 1 ? k_r2c_x<T, L, 2, true> : k_r2c_x<T, L, 2, false>;
+                k<<<grid, CS::NT, CS::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
             }
         } else {
             dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
-            k_r2c_x<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+            auto* k = geo_.G > 1 ? k_r2c_x<T, L, 0, true> : k_r2c_x<T, L, 0, false>;
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
         }
     });
     if (ev) ck(cudaEventRecord(ev[1], stream_), "event");
-    if (stop_after_ == 1) return;
-    if (yz()) {   // K2 + K3 + K4 in one kernel (thin / small grids)
+}
+
+// B: K2 (y forward) -> K3 (z, tensor product, inverse z) -> K4 (y inverse) on
+// this rank's x-bin block of every plane: Ar_ -> B_ -> Ar_ (Ar_ = A_ on one GPU)
+template <class T>
+void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
+    const Ctl ctl = make_ctl(it);
+    if (yz()) {   // K2 + K3 + K4 in one kernel (thin / small grids, one GPU)
+        if (stop_after_ >= 2 && stop_after_ <= 3) return;
         with_yz([&]<int LY, int LZ>() {
             using CF = YZCfg<T, LY, LZ>;
             k_fft_yz_small<T, LY, LZ><<<(geo_.Hx + CF::W - 1) / CF::W, CF::NT, CF::SMEM, stream_>>>(
                 geo_, A_, Kt_, tw_, ybuf_, ctl);
         });
+        if (ev) for (int q = 2; q <= 4; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
         return;
     }
-    if (k2_tma_) {
+    const bool work = geo_.Hv > 0;
+    if (work && k2_tma_) {
         with_pow2(Py_, [&]<int L>() {
             if constexpr (YTCfg<T, L>::OK) {
                 using CF = YTCfg<T, L>;
-                const int ntx = (geo_.Hx + CF::W - 1) / CF::W;
+                const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
                 auto* k = 2 * geo_.ny == L ? k_fft_y_fwd_tma<T, L, true> : k_fft_y_fwd_tma<T, L, false>;
                 k<<<k2_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmA_, B_, tw_, ctl, ntx, k2_box_);
             }
         });
-        return;
+    } else if (work) {
+        with_pow2(Py_, [&]<int L>() {
+            using CF = YCfg<T, L>;
+            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+            if (2 * geo_.ny == L)
+                k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
+            else
+                k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
+        });
     }
-    with_pow2(Py_, [&]<int L>() {
-        using CF = YCfg<T, L>;
-        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
-        if (2 * geo_.ny == L)
-            k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
-        else
-            k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, B_, tw_, ctl);
-    });
-}
-
-// B: K3 on the receive blocks Br_ (this rank's x-bin block, all z)
-template <class T>
-void Engine<T>::enq_B(const Iter& it) {
-    const Ctl ctl = make_ctl(it);
-    if (geo_.Hv <= 0 || yz()) return;
-    with_pow2(Pz_, [&]<int L>() {
+    if (ev) ck(cudaEventRecord(ev[2], stream_), "event");
+    if (stop_after_ == 2) return;
+    if (work) with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
             dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
-            k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, Br_, Kt_, ybuf_, ctl);
+            k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, B_, Kt_, ybuf_, ctl);
         } else if constexpr (z_variant<T, L>() == 2) {
             using CF = Z2Cfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
-            const bool fz = 2 * geo_.nzg == L, multi = geo_.G > 1;
-            auto* k = fz ? (multi ? k_fft_z_conv2<T, L, true, true> : k_fft_z_conv2<T, L, true, false>)
-                         : (multi ? k_fft_z_conv2<T, L, false, true> : k_fft_z_conv2<T, L, false, false>);
-            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
+            auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true> : k_fft_z_conv2<T, L, false>;
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
         } else {
             using CF = ZCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
-            k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Br_, Kt_, tw_, ybuf_, ctl);
+            k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
         }
     });
+    if (ev) ck(cudaEventRecord(ev[3], stream_), "event");
+    if (stop_after_ == 3) return;
+    if (work && k4_tma_) with_pow2(Py_, [&]<int L>() {
+        if constexpr (YICfg<T, L>::OK) {
+            using CF = YICfg<T, L>;
+            const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
+            auto* k = 2 * geo_.ny == L ? k_fft_y_inv_tma<T, L, true> : k_fft_y_inv_tma<T, L, false>;
+            k<<<k4_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, Ar_, tw_, ctl, ntx);
+        }
+    });
+    else if (work) with_pow2(Py_, [&]<int L>() {
+        using CF = YCfg<T, L>;
+        dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+        if (2 * geo_.ny == L)
+            k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
+        else
+            k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
+    });
+    if (ev) ck(cudaEventRecord(ev[4], stream_), "event");
 }
 
-// C: K4 (y inverse, send blocks -> A) + K5 (x inverse + H_eff + LLG + Euler)
+// C: K5 (x inverse + H_eff + LLG + Euler) on A_ (the receive side of the second transpose)
 template <class T>
 void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     const Ctl ctl = make_ctl(it);
@@ -530,43 +566,32 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     const long long nrows = (long long)geo_.ny * geo_.nz;
     const T* Mc = M_[cur];
     T* Mn = M_[cur ^ 1];
-    if (!yz() && k4_tma_) with_pow2(Py_, [&]<int L>() {
-        if constexpr (YICfg<T, L>::OK) {
-            using CF = YICfg<T, L>;
-            const int ntx = (geo_.Hx + CF::W - 1) / CF::W;
-            auto* k = 2 * geo_.ny == L ? k_fft_y_inv_tma<T, L, true> : k_fft_y_inv_tma<T, L, false>;
-            k<<<k4_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, A_, tw_, ctl, ntx);
-        }
-    });
-    else if (!yz()) with_pow2(Py_, [&]<int L>() {
-        using CF = YCfg<T, L>;
-        dim3 grid((geo_.Hx + CF::W - 1) / CF::W, geo_.nz, 3);
-        if (2 * geo_.ny == L)
-            k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
-        else
-            k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, A_, tw_, ctl);
-    });
-    if (ev) ck(cudaEventRecord(ev[4], stream_), "event");
-    if (stop_after_ == 4) return;
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
         if constexpr (L >= 2 && L <= 256) {
             if (small_x_) {   // one row per CTA (few-row grids such as SP4)
                 using CS = LCfg<T, L, 1>;
-                auto* k = io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 1, true> : k_c2r_x_llg_v<T, L, true, 1, false>)
-                                  : (fwd ? k_c2r_x_llg_v<T, L, false, 1, true> : k_c2r_x_llg_v<T, L, false, 1, false>);
+                auto* k = geo_.G > 1
+                              ? (io.sums ? k_c2r_x_llg_v<T, L, true, 1, false, true>
+                                         : k_c2r_x_llg_v<T, L, false, 1, false, true>)
+                          : io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 1, true> : k_c2r_x_llg_v<T, L, true, 1, false>)
+                                    : (fwd ? k_c2r_x_llg_v<T, L, false, 1, true> : k_c2r_x_llg_v<T, L, false, 1, false>);
                 k<<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
                 return;
             }
         }
+        const bool multi = geo_.G > 1;
         if (geo_.nx % V16<T>::V == 0) {
-            auto* k = io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 0, true> : k_c2r_x_llg_v<T, L, true, 0, false>)
+            auto* k = multi ? (io.sums ? k_c2r_x_llg_v<T, L, true, 0, false, true>
+                                       : k_c2r_x_llg_v<T, L, false, 0, false, true>)
+                    : io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 0, true> : k_c2r_x_llg_v<T, L, true, 0, false>)
                               : (fwd ? k_c2r_x_llg_v<T, L, false, 0, true> : k_c2r_x_llg_v<T, L, false, 0, false>);
             k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
-        } else
-            k_c2r_x_llg<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl,
-                                                                    hl);
+        } else {
+            auto* k = multi ? k_c2r_x_llg<T, L, true> : k_c2r_x_llg<T, L, false>;
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+        }
     });
 }
 
@@ -586,16 +611,15 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, b
             for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
     } else {
         enq_A(it, cur, events ? ev : nullptr, skip_k1);
-        if (events) ck(cudaEventRecord(ev[2], stream_), "event");
-        if (stop_after_ == 1 || stop_after_ == 2) return;
-        if (tr_ && slab_.world > 1) tr_->alltoall(B_, Br_, geo_.S_blk * sizeof(C2<T>), stream_);
-        enq_B(it);
-        if (events) ck(cudaEventRecord(ev[3], stream_), "event");
-        if (stop_after_ == 3) return;
-        if (tr_ && slab_.world > 1) tr_->alltoall(Br_, B_, geo_.S_blk * sizeof(C2<T>), stream_);
+        if (stop_after_ == 1) return;
+        // transpose #1: x-bin block p of every local plane -> rank p
+        if (tr_ && slab_.world > 1) tr_->alltoall(A_, Ar_, geo_.SA * sizeof(C2<T>), stream_);
+        enq_B(it, events ? ev : nullptr);
+        if (stop_after_ >= 2 && stop_after_ <= 4) return;
+        // transpose #2 (inverse): back to this rank's planes, all x-bins
+        if (tr_ && slab_.world > 1) tr_->alltoall(Ar_, A_, geo_.SA * sizeof(C2<T>), stream_);
         enq_C(it, cur, events ? ev : nullptr, fwd);
         if (events) ck(cudaEventRecord(ev[5], stream_), "event");
-        if (stop_after_ == 4) return;
     }
     if (tr_ && slab_.world > 1) {
         tr_->allreduce_max_u64(torque_ + it.slot, 1, stream_);

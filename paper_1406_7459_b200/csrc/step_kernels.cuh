@@ -61,26 +61,40 @@ template <class T, int L> struct ZCfg {   // K3
 };
 
 // Geometry of one rank's share of the problem.  Single GPU: G = 1, the slab
-// is the whole grid and the spectral layout is [1][3][nz][Py][Hp].
+// is the whole grid, A is [3][nz][ny][Hp] and B is [3][nz][Py][Hp].
 // z-slab decomposition over G ranks: the rank owns
-// planes [k0, k0+nz) of nzg for the x/y passes and the LLG update, and x-bin
-// block `ublk` (width Wb, Hv valid) of every z column for the z pass.  The
-// y-spectrum B is laid out [block][3][nz][Py][Wb]: block b of the send side
-// goes to rank b, block g of the receive side came from rank g, so the two
-// all-to-all transposes move contiguous blocks and no pack kernel exists.
+// planes [k0, k0+nz) of nzg for the x passes (K1, K5) and the LLG update, and
+// x-bin block `ublk` (width Wb, Hv valid) of every plane for the y and z
+// passes (K2-K4).  The transposes sit right after K1 / before K5, where the
+// spectrum has ny (not Py) rows, so they move half the bytes of a transpose
+// after the y pass.  A is laid out [block][3][nz][ny][Wb] (row pitch Hp = Wb):
+// block b of the send side goes to rank b, block g of the receive side came
+// from rank g (planes g*nz ...), so both all-to-alls move contiguous blocks and
+// no pack kernel exists.  B = [3][nzg][Py][Wb] is then rank-local.
 struct Geo {
     int nx, ny, nz;       // nz: planes of this rank's slab
     int Px, Py, Pz;       // Pz from the global nzg
     int N;                // Px/2 complex points per x row
     int Hx;               // N + 1 bins
-    int Hp;               // pitch of A rows
+    int Hp;               // pitch of A rows (= Wb when G > 1)
     long long ncell;      // cells of the slab
     int nzg, k0;          // global planes, first plane of the slab
     int G, ublk, Wb, Hv;  // ranks, this rank's x-bin block, block width, valid bins in it
-    long long S_blk, S_c, S_k;   // B strides: block, component, plane (row stride Wb)
+    long long SA;         // A block stride (3 nz ny Hp; one block when G == 1)
+    unsigned binv;        // ceil(2^24 / Wb): x-bin u -> block (u * binv) >> 24
+    long long S_c, S_k;   // B strides: component (nzg planes), plane (row stride Wb)
     int pf1, pf5;         // L2 prefetch distance of K1 / K5 in CTAs (~resident CTAs; 0 = off)
     int pfm;              // prefetch mask: 1 K1 ahead, 2 K5 own M rows, 4 K5 spectrum ahead
 };
+
+// Round a shared-memory pointer up to 128 bytes (TMA destinations).  The offset
+// is added to the shared pointer itself, so the compiler keeps shared-space
+// addressing (LDS/STS); an integer round trip would degrade it to generic LD/ST.
+template <class P>
+__device__ __forceinline__ P* align128(P* p) {
+    const unsigned pad = (128u - (smem_u32(p) & 127u)) & 127u;
+    return reinterpret_cast<P*>(reinterpret_cast<unsigned char*>(p) + pad);
+}
 
 // Asynchronous L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch, TMA
 // unit: no registers, no shared memory).  Trimmed inward to 16-byte bounds.
@@ -90,16 +104,23 @@ __device__ __forceinline__ void l2_prefetch(const void* p, long long bytes) {
     if (e <= a) return;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
-// z offset of global plane k in the receive-side layout (rank k / nz, plane k % nz).
-__device__ __forceinline__ long long zoff(const Geo& g, int k) {
-    if (g.G == 1) return (long long)k * g.S_k;
-    return (long long)(k / g.nz) * g.S_blk + (long long)(k % g.nz) * g.S_k;
+// Element of x-bin u in the A row at in-block offset rowoff.  Single GPU: one
+// block.  Slab decomposition (MULTI): bin u sits in the block of rank u / Wb at
+// column u % Wb (the division as a 24-bit reciprocal multiply, exact for u < 2^12).
+template <bool MULTI, class P>
+__device__ __forceinline__ P* abin(const Geo& g, P* A, long long rowoff, int u) {
+    if constexpr (!MULTI) {
+        return A + rowoff + u;
+    } else {
+        const int b = (int)(((unsigned)u * g.binv) >> 24);
+        return A + b * g.SA + rowoff + (u - b * g.Wb);
+    }
 }
-// Same with the single-GPU case resolved at compile time (no division code).
-template <bool MULTI>
-__device__ __forceinline__ long long zoff_t(const Geo& g, int k) {
-    if constexpr (!MULTI) return (long long)k * g.S_k;
-    else return (long long)(k / g.nz) * g.S_blk + (long long)(k % g.nz) * g.S_k;
+// Offset of the A row (component comp, global plane k, row j) seen by the y
+// passes on the receive side: plane k came from rank k / nz.
+__device__ __forceinline__ long long arow_y(const Geo& g, int comp, int k, int j) {
+    const int kb = k / g.nz, kl = k - kb * g.nz;
+    return kb * g.SA + ((long long)(comp * g.nz + kl) * g.ny + j) * g.Hp;
 }
 // One-plane M halos below / above the slab ([3][ny][nx] each; null at the
 // global boundary or on a single GPU).
@@ -138,7 +159,7 @@ __device__ __forceinline__ void r2c_post(const C2<T>* scol, C2<T>* dst, int k, C
 }
 
 // ------------------------------------------------------------------ K1
-template <class T, int N, int RS = 0>
+template <class T, int N, int RS = 0, bool MULTI = false>
 __global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
 k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = XCfg<T, N, RS>;
@@ -192,9 +213,9 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
         const C2<T> d = csub<T>(zk, zn);
         const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
         const C2<T> wo = cmul<T>(w, O);
-        C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
-        dst[k] = cadd<T>(E, wo);
-        if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
+        const long long ro = ((long long)comp * nrows + row0 + col) * g.Hp;
+        *abin<MULTI>(g, A, ro, k) = cadd<T>(E, wo);
+        if (N - k != k) *abin<MULTI>(g, A, ro, N - k) = cconj<T>(csub<T>(E, wo));
     };
     constexpr int HP = N / 2 > 0 ? N / 2 : 1;
     const int rows = (int)(nrows - row0 < ROWS ? nrows - row0 : ROWS);
@@ -326,10 +347,9 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
-    const int k = blockIdx.y, comp = blockIdx.z;
-    const C2<T>* src = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
-    // tiles never straddle a block: Wb is a multiple of 16 >= W
-    C2<T>* dst = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
+    const int k = blockIdx.y, comp = blockIdx.z;   // k: global plane
+    const C2<T>* src = A + arow_y(g, comp, k, 0) + u0;
+    C2<T>* dst = B + comp * g.S_c + k * g.S_k + u0;
     const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
     auto ld0 = [&](int col, int pos) -> C2<T> {
         if (!FY && pos >= ny) return mk<T>(0, 0);
@@ -367,9 +387,9 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* work = reinterpret_cast<C2<T>*>(smem_raw);
     // TMA destinations must be 128-byte aligned
-    C2<T>* stage = reinterpret_cast<C2<T>*>((reinterpret_cast<uintptr_t>(work + W * L) + 127) & ~uintptr_t(127));
+    C2<T>* stage = align128(work + W * L);
     __shared__ uint64_t bar;
-    const int ny = g.ny, nz = g.nz, Wb = g.Wb;
+    const int ny = g.ny, nz = g.nzg, Wb = g.Wb;   // all planes of this rank's x-bin block
     const int ntiles = ntx * nz * 3;
     int t = blockIdx.x;
     if (t >= ntiles) return;
@@ -381,7 +401,8 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     __syncthreads();
     auto issue = [&](int tt) {   // one thread
         const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
-        const int row0 = (comp * nz + k) * ny;
+        const int kb = k / g.nz, kl = k - kb * g.nz;   // plane k came from rank kb
+        const int row0 = ((kb * 3 + comp) * g.nz + kl) * ny;
         mbar_arrive_expect_tx(&bar, (unsigned)(ny * W * CF::CS));
         for (int r = 0; r < ny; r += box_rows)
             tma_load_2d(stage + r * W, &tmA, bx * W * (CF::CS / 8), row0 + r, &bar);
@@ -398,7 +419,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     for (; t < ntiles; t += gridDim.x) {
         const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
         const int u0 = bx * W;
-        C2<T>* dst = B + (u0 / Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % Wb;
+        C2<T>* dst = B + comp * g.S_c + k * g.S_k + u0;
         auto stn = [&](int col, int pos, C2<T> v) { dst[pos * Wb + col] = v; };
         mbar_wait(&bar, parity);
         parity ^= 1;
@@ -423,9 +444,9 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
-    const int k = blockIdx.y, comp = blockIdx.z;
-    const C2<T>* src = B + (u0 / g.Wb) * g.S_blk + comp * g.S_c + k * g.S_k + u0 % g.Wb;
-    C2<T>* dst = A + ((long long)comp * g.nz + k) * g.ny * g.Hp + u0;
+    const int k = blockIdx.y, comp = blockIdx.z;   // k: global plane
+    const C2<T>* src = B + comp * g.S_c + k * g.S_k + u0;
+    C2<T>* dst = A + arow_y(g, comp, k, 0) + u0;
     const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
     auto ld0 = [&](int col, int pos) -> C2<T> { return src[pos * Wb + col]; };
     auto lds = [&](int col, int pos) -> C2<T> { return sm[yswz<T, L, W>(pos) * W + col]; };
@@ -459,11 +480,13 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
                 const C2<T>* __restrict__ tw, Ctl ctl, int ntx) {
     using CF = YICfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT, HALF = CF::HALF;
+    // lets the compiler resolve every gather's half (slot) at compile time
+    __builtin_assume(threadIdx.x < (unsigned)NT);
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C2<T>* slot0 = reinterpret_cast<C2<T>*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    C2<T>* slot0 = align128(reinterpret_cast<C2<T>*>(smem_raw));
     __shared__ uint64_t bar[3];
-    const int ny = g.ny, nz = g.nz, Hp = g.Hp, Wb = g.Wb;
+    const int ny = g.ny, nz = g.nzg, Hp = g.Hp;   // all planes of this rank's x-bin block
     const int ntiles = ntx * nz * 3;
     if ((int)blockIdx.x >= ntiles) return;
     // fill f = 2 i + h (tile i of this CTA, half h) -> slot f % 3, phase (f / 3) & 1
@@ -472,11 +495,11 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
         if (tt >= ntiles) return;
         const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
         const int u0 = bx * W;
-        const long long row0 = (((long long)(u0 / Wb) * 3 + comp) * nz + k) * L + h * HALF;
+        const long long row0 = ((long long)comp * nz + k) * L + h * HALF;
         const int s = (2 * i + h) % 3;
         mbar_arrive_expect_tx(&bar[s], (unsigned)CF::SLOT);
         for (int r = 0; r < HALF; r += CF::BOX)
-            tma_load_2d(slot0 + s * (HALF * W) + r * W, &tmB, (u0 % Wb) * (CF::CS / 8), (int)(row0 + r), &bar[s]);
+            tma_load_2d(slot0 + s * (HALF * W) + r * W, &tmB, u0 * (CF::CS / 8), (int)(row0 + r), &bar[s]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < 3; ++s) mbar_init(&bar[s], 1);
@@ -493,28 +516,59 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
         const int u0 = bx * W;
         C2<T>* sa = slot0 + ((2 * i) % 3) * (HALF * W);
         C2<T>* sb = slot0 + ((2 * i + 1) % 3) * (HALF * W);
-        auto at = [&](int col, int pos) -> C2<T>& { return (pos < HALF ? sa : sb)[(pos & (HALF - 1)) * W + col]; };
-        auto lds = [&](int col, int pos) -> C2<T> { return at(col, pos); };
-        auto sts = [&](int col, int pos, C2<T> v) { at(col, pos) = v; };
-        C2<T>* dst = A + ((long long)comp * nz + k) * ny * Hp + u0;
+        C2<T>* dst = A + arow_y(g, comp, k, 0) + u0;
         auto stn = [&](int col, int pos, C2<T> v) {
             if (FY || pos < ny) dst[pos * Hp + col] = v;
         };
         mbar_wait(&bar[(2 * i) % 3], ((2 * i) / 3) & 1);
         mbar_wait(&bar[(2 * i + 1) % 3], ((2 * i + 1) / 3) & 1);
         // transposed stage 1: in place, per task (no barrier between gather and scatter)
-        fft_stage<T, L, 1, true, W, NT, true, false>(lds, sts, tw);
+        // transposed stage 1 (MP = 1, no twiddles): task p owns rows p*R1 .. p*R1+R1-1,
+        // all in one slot; in place, so no barrier between gather and scatter
+        {
+            constexpr int R0s = Plan<T, L>::R0, R1 = Plan<T, L>::R1, TPT1 = (W * R0s + NT - 1) / NT;
+            static_assert((W * R0s) % NT == 0 && R0s * R1 == L, "two-stage plan, whole tasks per thread");
+#pragma unroll
+            for (int q = 0; q < TPT1; ++q) {
+                const int e = threadIdx.x + q * NT, col = e % W, p = e / W;
+                C2<T>* b = (2 * p < R0s ? sa + p * R1 * W : sb + (p * R1 - HALF) * W) + col;
+                C2<T> x[R1];
+#pragma unroll
+                for (int j = 0; j < R1; ++j) x[j] = b[j * W];
+                dft<T, R1, true>(x);
+#pragma unroll
+                for (int j = 0; j < R1; ++j) b[j * W] = x[j];
+            }
+        }
         __syncthreads();
-        // transposed stage 0: gather (all rows), barrier, then refill both slots
-        // while this tile's DFTs and HBM stores run
-        fft_stage<T, L, 0, true, W, NT, true, true, false, true, false, L>(
-            lds, stn, tw, [&] {
-                if (threadIdx.x == 0) {
-                    fence_proxy_async_smem();
-                    issue(i + 1, 1);
-                    issue(i + 2, 0);
-                }
-            });
+        // transposed stage 0 (task n2 gathers rows n2 + MP*j: j < R0/2 in the
+        // first slot, the rest in the second, resolved at compile time): gather,
+        // barrier, refill both slots while this tile's DFTs and HBM stores run
+        constexpr int R0 = Plan<T, L>::R0, MP = L / R0, TPT = (W * MP + NT - 1) / NT;
+        static_assert((W * MP) % NT == 0, "whole tasks per thread");
+        C2<T> v[TPT][R0];
+#pragma unroll
+        for (int q = 0; q < TPT; ++q) {
+            const int e = threadIdx.x + q * NT, col = e % W, n2 = e / W;
+#pragma unroll
+            for (int j = 0; j < R0; ++j)
+                v[q][j] = 2 * j < R0 ? sa[(n2 + MP * j) * W + col] : sb[(n2 + MP * j - HALF) * W + col];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            issue(i + 1, 1);
+            issue(i + 2, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < TPT; ++q) {
+            const int e = threadIdx.x + q * NT, col = e % W, n2 = e / W;
+#pragma unroll
+            for (int k = 1; k < R0; ++k) v[q][k] = cmulc<T>(v[q][k], tw_lookup<T, L, L>(tw, n2 * k));
+            dft<T, R0, true, false, true>(v[q]);
+#pragma unroll
+            for (int j = 0; 2 * j < R0; ++j) stn(col, n2 + MP * j, v[q][j]);
+        }
     }
 }
 
@@ -541,7 +595,7 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
     // column c = comp*2W + r*W + w  (r: 0 -> v, 1 -> Py-v)
     auto gaddr = [&](int col, int pos) -> long long {
         const int comp = col / (2 * W), r = (col / W) & 1, w = col % W;
-        return comp * g.S_c + zoff(g, pos) + (r ? rowB : rowA) * Wb + u0 + w;
+        return comp * g.S_c + (long long)pos * g.S_k + (r ? rowB : rowA) * Wb + u0 + w;
     };
     auto valid = [&](int col) { return u0 + (col % W) < Hv && (pair || ((col / W) & 1) == 0); };
     auto ld0 = [&](int col, int pos) -> C2<T> {
@@ -656,8 +710,7 @@ template <class T, int L> struct Z2Cfg {
 
 // FZ: nz == Pz/2, so the pruned first/last stages never meet a plane >= nz.
 // Padding x-bins (>= Hv, inside the block pitch) are computed, not masked.
-// MULTI: z-slab decomposition (planes spread over the receive blocks).
-template <class T, int L, bool FZ, bool MULTI = false>
+template <class T, int L, bool FZ>
 __global__ void __launch_bounds__(Z2Cfg<T, L>::NT, Z2Cfg<T, L>::MINB)
 k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
               const int* __restrict__ ybuf, Ctl ctl) {
@@ -689,7 +742,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int j = 0; j < R0 / 2; ++j) {
             const int pos = R1 * j + n2;
-            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + zoff_t<MULTI>(g, pos)] : mk<T>(0, 0);
+            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + (long long)pos * g.S_k] : mk<T>(0, 0);
         }
     };
     fetch(0);
@@ -773,7 +826,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
             for (int j = 0; 2 * j < R0; ++j) {
                 const int pos = R1 * j + n2;
-                if (FZ || pos < nz) gcol[c * cstride + zoff_t<MULTI>(g, pos)] = x[j];
+                if (FZ || pos < nz) gcol[c * cstride + (long long)pos * g.S_k] = x[j];
             }
         }
     }
@@ -807,7 +860,7 @@ k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int*
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int k = 0; k < L; ++k) x[c][k] = (k < nz && 2 * k < L) ? base[c * cstride + zoff(g, k)] : mk<T>(0, 0);
+        for (int k = 0; k < L; ++k) x[c][k] = (k < nz && 2 * k < L) ? base[c * cstride + (long long)k * g.S_k] : mk<T>(0, 0);
 #pragma unroll
     for (int c = 0; c < 3; ++c) dft<T, L, false, true>(x[c]);
     const int Hz = L / 2 + 1;
@@ -824,7 +877,7 @@ k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int*
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int k = 0; k < L; ++k)
-            if (k < nz && 2 * k < L) base[c * cstride + zoff(g, k)] = x[c][k];
+            if (k < nz && 2 * k < L) base[c * cstride + (long long)k * g.S_k] = x[c][k];
 }
 
 // ------------------------------------------------------------ K2+K3+K4
@@ -1095,7 +1148,7 @@ __device__ __forceinline__ void block_finish(const StepIO& io, const Ctl& ctl, d
     if (lane == 0) *io.ticket = 0;
 }
 
-template <class T, int N>
+template <class T, int N, bool MULTI = false>
 __global__ void __launch_bounds__(LCfg<T, N>::NT, LCfg<T, N>::MINB)
 k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
             T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io,
@@ -1116,9 +1169,9 @@ k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __re
         const long long row = row0 + r;
         C2<T> a = mk<T>(0, 0), b = mk<T>(0, 0);
         if (row < nrows) {
-            const C2<T>* src = A + ((long long)comp * nrows + row) * g.Hp;
-            a = src[k];
-            b = src[N - k];
+            const long long ro = ((long long)comp * nrows + row) * g.Hp;
+            a = *abin<MULTI>(g, A, ro, k);
+            b = *abin<MULTI>(g, A, ro, N - k);
         }
         const C2<T> w = __ldg(tw_dense<T, 2 * N>(tw) + k);   // W_Px^k, used conjugated
         {
@@ -1418,7 +1471,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 // while they are in shared memory, writing A in place of the spectrum this
 // CTA consumed (only its own rows: no cross-CTA hazard).  Saves K1's M read
 // and launch on every step but the first of a graph chunk.
-template <class T, int N, bool SUMS, int RS = 0, bool FWD = false>
+template <class T, int N, bool SUMS, int RS = 0, bool FWD = false, bool MULTI = false>
 __global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
 k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
               T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
@@ -1467,10 +1520,10 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
         const long long row = row0 + col % ROWS;
         pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
         if (e < ITEMS && row < nrows) {
-            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
-            pa[it] = src[k];
-            pb[it] = src[N - k];
-            if (k == 0 && N > 1) pc[it] = src[N / 2];
+            const long long ro = ((long long)(col / ROWS) * nrows + row) * g.Hp;
+            pa[it] = *abin<MULTI>(g, A, ro, k);
+            pb[it] = *abin<MULTI>(g, A, ro, N - k);
+            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, A, ro, N / 2);
         }
     }
     auto pre = [&](C2<T>* scol, int k, C2<T> a, C2<T> b) {

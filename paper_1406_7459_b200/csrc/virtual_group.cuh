@@ -168,8 +168,8 @@ private:
         }
     }
 
-    // One iteration of all ranks: halo -> A -> all-to-all -> B -> all-to-all
-    // -> C, then the torque max / error / sums combined on the host.
+    // One iteration of all ranks: halo -> A (K1) -> all-to-all -> B (K2-K4) ->
+    // all-to-all -> C (K5), then the torque max / error / sums combined on the host.
     void iterate(Iter it, double* torque = nullptr, bool* bad = nullptr, double* sums = nullptr) {
         it.slot = 0;
         it.check_prev = 0;
@@ -226,13 +226,13 @@ private:
 
     // forward: send block p of rank r -> receive block r of rank p; backward: the reverse.
     void exchange(bool forward) {
-        const size_t blk = ranks_[0]->geo_.S_blk * sizeof(C2<T>);
+        const size_t blk = ranks_[0]->geo_.SA * sizeof(C2<T>);
         for (int r = 0; r < world_; ++r)
             for (int p = 0; p < world_; ++p) {
                 Engine<T>& a = *ranks_[r];
                 Engine<T>& b = *ranks_[p];
-                const char* src = reinterpret_cast<const char*>(forward ? a.B_ : a.Br_) + p * blk;
-                char* dst = reinterpret_cast<char*>(forward ? b.Br_ : b.B_) + r * blk;
+                const char* src = reinterpret_cast<const char*>(forward ? a.A_ : a.Ar_) + p * blk;
+                char* dst = reinterpret_cast<char*>(forward ? b.Ar_ : b.A_) + r * blk;
                 ck(cudaMemcpyAsync(dst, src, blk, cudaMemcpyDeviceToDevice, stream_), "all-to-all");
             }
     }

@@ -2,10 +2,11 @@
 
 Two processes run the z-slab algorithm of the engine in numpy with the exact
 block layout of the device path (paper_1406_7459_b200/decomposition.py ==
-csrc Slab/Geo): local x (R2C) and y FFTs on the slab, pack into
-[block][3][nzl][Py][Wb], all_to_all, z FFT + tensor product on the rank's
-x-bin block, all_to_all back, inverse y / x; and the one-plane M halo for the
-exchange stencil.  The gathered fields must equal the single-process oracle.
+csrc Slab/Geo): local x (R2C) FFT on the slab into [block][3][nzl][ny][Wb],
+all_to_all, y FFT + z FFT + tensor product + inverse z / y on the rank's
+x-bin block of every plane, all_to_all back, inverse x; and the one-plane M
+halo for the exchange stencil.  The gathered fields must equal the
+single-process oracle.
 """
 import os
 import socket
@@ -69,19 +70,18 @@ def worker(rank, world, port, m, out_path):
     Kf = full_kernel_spectrum(*GRID)
     M = m.reshape(3, nz, ny, nx)[:, sl.k0:sl.k0 + sl.nzl]          # this rank's slab
 
-    # K1 + K2 on the slab, packed by destination block
+    # K1 on the slab, packed by destination block (bin u -> block_of(u))
     A = np.fft.rfft(M, n=px, axis=3)                               # [3][nzl][ny][Hx]
-    By = np.fft.fft(A, n=py, axis=2)                               # [3][nzl][Py][Hx]
-    send = np.zeros((world, 3, sl.nzl, py, bl.Wb), complex)
-    for p in range(world):
-        hv = bl.valid(p)
-        send[p, ..., :hv] = By[..., p * bl.Wb:p * bl.Wb + hv]
+    send = np.zeros((world, 3, sl.nzl, ny, bl.Wb), complex)
+    for u in range(bl.Hx):
+        p = bl.block_of(u)
+        send[p, ..., u - p * bl.Wb] = A[..., u]
     recv = alltoall(send, world)                                   # block g: planes of rank g
 
-    # K3 on this rank's x-bin block: full z columns
+    # K2 + K3 + K4 on this rank's x-bin block of every plane
     hv, u0 = bl.valid(rank), rank * bl.Wb
-    Z = np.concatenate([recv[g] for g in range(world)], axis=1)    # [3][nz][Py][Wb]
-    Zf = np.fft.fft(Z, n=pz, axis=1)
+    Z = np.concatenate([recv[g] for g in range(world)], axis=1)    # [3][nz][ny][Wb]
+    Zf = np.fft.fft(np.fft.fft(Z, n=py, axis=2), n=pz, axis=1)     # [3][Pz][Py][Wb]
     k = Kf[:, :, :, u0:u0 + hv]
     xx, yy, zz, xy, xz, yz = k
     a, b, c = Zf[0, ..., :hv], Zf[1, ..., :hv], Zf[2, ..., :hv]
@@ -89,17 +89,16 @@ def worker(rank, world, port, m, out_path):
     H[0, ..., :hv] = xx * a + xy * b + xz * c
     H[1, ..., :hv] = xy * a + yy * b + yz * c
     H[2, ..., :hv] = xz * a + yz * b + zz * c
-    Hz = np.fft.ifft(H, axis=1)[:, :nz] * pz
-    back = np.stack([Hz[:, g * sl.nzl:(g + 1) * sl.nzl] for g in range(world)])
+    Hyz = (np.fft.ifft(np.fft.ifft(H, axis=1)[:, :nz] * pz, axis=2) * py)[:, :, :ny]
+    back = np.stack([Hyz[:, g * sl.nzl:(g + 1) * sl.nzl] for g in range(world)])
     mine = alltoall(back, world)                                   # block p: my planes, x-bins of rank p
 
-    # K4 + K5 (demag part) on the slab
-    Hs = np.zeros((3, sl.nzl, py, bl.Hx), complex)
+    # K5 (demag part) on the slab
+    Hs = np.zeros((3, sl.nzl, ny, bl.Hx), complex)
     for p in range(world):
         hvp = bl.valid(p)
         Hs[..., p * bl.Wb:p * bl.Wb + hvp] = mine[p, ..., :hvp]
-    Ay = (np.fft.ifft(Hs, axis=2) * py)[:, :, :ny]
-    hd = np.fft.irfft(Ay, n=px, axis=3)[..., :nx] * px / (px * py * pz)
+    hd = np.fft.irfft(Hs, n=px, axis=3)[..., :nx] * px / (px * py * pz)
 
     # one-plane halo of M for the exchange stencil (Neumann at the global ends)
     lo = np.zeros((3, ny, nx))
@@ -174,9 +173,15 @@ def test_partition_math_matches_device_rules():
     assert sum(b.valid(r) for r in range(8)) == 513
     assert b.Wb % 16 == 0 and 8 * b.Wb >= b.Hx
     one = D.blocks(512, 512, 64, 1)
-    assert one.Wb == 528 and one.S_c == 64 * 1024 * 528     # single GPU: today's [3][nz][Py][Hp]
+    assert one.Wb == 528 and one.S_c == 64 * 1024 * 528     # single GPU: [3][nz][Py][Hp]
+    assert one.SA == 3 * 64 * 512 * 528                     # single GPU: A = [3][nz][ny][Hp]
+    # the device's reciprocal block index equals u // Wb for every bin
+    for G in (2, 4, 8):
+        for n in (16, 100, 512, 1024, 2048):
+            bb = D.blocks(n, 8, 8 * G, G)
+            assert all(bb.block_of(u) == u // bb.Wb for u in range(bb.Hx))
     with pytest.raises(ValueError, match="divisible"):
         D.slab(64, 0, 3)
     # per-rank transpose volume at 8 GPUs, fp32: 2 transposes x 7 remote blocks of
-    # 3*nzl*Py*Wb complex (the y-spectrum is moved)
-    assert D.alltoall_bytes_per_rank(512, 512, 64, 8) == 2 * 7 * 3 * 8 * 1024 * 80 * 8
+    # 3*nzl*ny*Wb complex (the x-spectrum is moved)
+    assert D.alltoall_bytes_per_rank(512, 512, 64, 8) == 2 * 7 * 3 * 8 * 512 * 80 * 8
