@@ -107,13 +107,14 @@ __device__ __forceinline__ void l2_prefetch(const void* p, long long bytes) {
 // Element of x-bin u in the A row at in-block offset rowoff.  Single GPU: one
 // block.  Slab decomposition (MULTI): bin u sits in the block of rank u / Wb at
 // column u % Wb (the division as a 24-bit reciprocal multiply, exact for u < 2^12).
+// rowp = A + rowoff (the row in block 0).
 template <bool MULTI, class P>
-__device__ __forceinline__ P* abin(const Geo& g, P* A, long long rowoff, int u) {
+__device__ __forceinline__ P* abin(const Geo& g, P* rowp, int u) {
     if constexpr (!MULTI) {
-        return A + rowoff + u;
+        return rowp + u;
     } else {
         const int b = (int)(((unsigned)u * g.binv) >> 24);
-        return A + b * g.SA + rowoff + (u - b * g.Wb);
+        return rowp + (b * g.SA + (u - b * g.Wb));
     }
 }
 // Offset of the A row (component comp, global plane k, row j) seen by the y
@@ -213,9 +214,9 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
         const C2<T> d = csub<T>(zk, zn);
         const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);   // -i/2 (zk - zn)
         const C2<T> wo = cmul<T>(w, O);
-        const long long ro = ((long long)comp * nrows + row0 + col) * g.Hp;
-        *abin<MULTI>(g, A, ro, k) = cadd<T>(E, wo);
-        if (N - k != k) *abin<MULTI>(g, A, ro, N - k) = cconj<T>(csub<T>(E, wo));
+        C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
+        *abin<MULTI>(g, dst, k) = cadd<T>(E, wo);
+        if (N - k != k) *abin<MULTI>(g, dst, N - k) = cconj<T>(csub<T>(E, wo));
     };
     constexpr int HP = N / 2 > 0 ? N / 2 : 1;
     const int rows = (int)(nrows - row0 < ROWS ? nrows - row0 : ROWS);
@@ -460,28 +461,35 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
 // K4 with TMA-staged input (two-stage plans): persistent CTAs over a ring of
 // three half-tile slots.  Tile i (L rows x W bins of B) lands as two halves in
 // slots (2i) % 3 and (2i+1) % 3.  The transposed first inverse stage (stage 1,
-// MP = 1) reads and writes the L/R0 contiguous rows of its task in place, so it
+// MP = 1) reads and writes the R1 contiguous rows of its task in place, so it
 // needs no second buffer; once the last stage has gathered the tile into
 // registers both its slots are free and the next tile's second half and the
 // tile after that's first half are issued into them, so every load is in
-// flight for at least one stage of compute.  Same arithmetic as k_fft_y_inv.
+// flight for at least one stage of compute.  Tiles are 128 bytes wide (16 f32
+// bins): a stage-1 task row then spans all 32 banks, so the tasks of a warp
+// never share a bank wavefront (with 64-byte rows the tasks, R1 rows apart,
+// collide 2-way and TMA destinations cannot be padded off the 128-byte grid).
+// Same arithmetic as k_fft_y_inv.
 template <class T, int L> struct YICfg {
-    static constexpr int W = YCfg<T, L>::W, NT = YCfg<T, L>::NT, CS = sizeof(C2<T>);
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr int W = 128 / CS;                        // 128-byte tile rows
+    static constexpr int NT = clampNT(W * L / regE<T>());
+    static constexpr int MINB = NT >= 512 ? 1 : 2;
+    static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
     static constexpr int HALF = L / 2;                        // rows per slot
-    static constexpr int SLOT = HALF * W * CS;
-    static constexpr int SMEM = 3 * SLOT + 128;               // + TMA alignment
+    static constexpr int SLOTE = HALF * W;                    // slot size in elements
+    static constexpr int SLOT = SLOTE * CS;                   // bytes per slot
     static constexpr int BOX = HALF < 256 ? HALF : 256;       // TMA box rows (<= 256)
-    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 110 * 1024 && L >= 256 && W * CS >= 16;
+    static constexpr int SMEM = 3 * SLOT + 128;               // + TMA alignment
+    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 200 * 1024 && L >= 256;
 };
 
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YICfg<T, L>::NT, 2)
+__global__ void __launch_bounds__(YICfg<T, L>::NT, YICfg<T, L>::MINB)
 k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restrict__ A,
                 const C2<T>* __restrict__ tw, Ctl ctl, int ntx) {
     using CF = YICfg<T, L>;
-    constexpr int W = CF::W, NT = CF::NT, HALF = CF::HALF;
-    // lets the compiler resolve every gather's half (slot) at compile time
-    __builtin_assume(threadIdx.x < (unsigned)NT);
+    constexpr int W = CF::W, NT = CF::NT, R0 = CF::R0, R1 = CF::R1, HALF = CF::HALF;
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* slot0 = align128(reinterpret_cast<C2<T>*>(smem_raw));
@@ -495,11 +503,11 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
         if (tt >= ntiles) return;
         const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
         const int u0 = bx * W;
-        const long long row0 = ((long long)comp * nz + k) * L + h * HALF;
+        const int row0 = (comp * nz + k) * L + h * CF::HALF;
         const int s = (2 * i + h) % 3;
         mbar_arrive_expect_tx(&bar[s], (unsigned)CF::SLOT);
         for (int r = 0; r < HALF; r += CF::BOX)
-            tma_load_2d(slot0 + s * (HALF * W) + r * W, &tmB, u0 * (CF::CS / 8), (int)(row0 + r), &bar[s]);
+            tma_load_2d(slot0 + s * CF::SLOTE + r * W, &tmB, u0 * (CF::CS / 8), row0 + r, &bar[s]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < 3; ++s) mbar_init(&bar[s], 1);
@@ -514,24 +522,23 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
         if (t >= ntiles) break;
         const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
         const int u0 = bx * W;
-        C2<T>* sa = slot0 + ((2 * i) % 3) * (HALF * W);
-        C2<T>* sb = slot0 + ((2 * i + 1) % 3) * (HALF * W);
+        C2<T>* sa = slot0 + ((2 * i) % 3) * CF::SLOTE;
+        C2<T>* sb = slot0 + ((2 * i + 1) % 3) * CF::SLOTE;
         C2<T>* dst = A + arow_y(g, comp, k, 0) + u0;
         auto stn = [&](int col, int pos, C2<T> v) {
             if (FY || pos < ny) dst[pos * Hp + col] = v;
         };
         mbar_wait(&bar[(2 * i) % 3], ((2 * i) / 3) & 1);
         mbar_wait(&bar[(2 * i + 1) % 3], ((2 * i + 1) / 3) & 1);
-        // transposed stage 1: in place, per task (no barrier between gather and scatter)
-        // transposed stage 1 (MP = 1, no twiddles): task p owns rows p*R1 .. p*R1+R1-1,
-        // all in one slot; in place, so no barrier between gather and scatter
+        // transposed stage 1 (MP = 1, no twiddles): task p owns rows p*R1 ..
+        // p*R1+R1-1, all in one slot; in place, so no barrier between gather and scatter
         {
-            constexpr int R0s = Plan<T, L>::R0, R1 = Plan<T, L>::R1, TPT1 = (W * R0s + NT - 1) / NT;
-            static_assert((W * R0s) % NT == 0 && R0s * R1 == L, "two-stage plan, whole tasks per thread");
+            constexpr int TPT1 = (W * R0 + NT - 1) / NT;
+            static_assert((W * R0) % NT == 0 && R0 * R1 == L, "two-stage plan, whole tasks per thread");
 #pragma unroll
             for (int q = 0; q < TPT1; ++q) {
                 const int e = threadIdx.x + q * NT, col = e % W, p = e / W;
-                C2<T>* b = (2 * p < R0s ? sa + p * R1 * W : sb + (p * R1 - HALF) * W) + col;
+                C2<T>* b = (2 * p < R0 ? sa + p * R1 * W : sb + (p * R1 - HALF) * W) + col;
                 C2<T> x[R1];
 #pragma unroll
                 for (int j = 0; j < R1; ++j) x[j] = b[j * W];
@@ -541,10 +548,10 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
             }
         }
         __syncthreads();
-        // transposed stage 0 (task n2 gathers rows n2 + MP*j: j < R0/2 in the
-        // first slot, the rest in the second, resolved at compile time): gather,
-        // barrier, refill both slots while this tile's DFTs and HBM stores run
-        constexpr int R0 = Plan<T, L>::R0, MP = L / R0, TPT = (W * MP + NT - 1) / NT;
+        // transposed stage 0: task n2 gathers rows n2 + MP*j (j < R0/2 in the
+        // first slot, resolved at compile time), barrier, refill both slots
+        // while this tile's DFTs and HBM stores run
+        constexpr int MP = L / R0, TPT = (W * MP + NT - 1) / NT;
         static_assert((W * MP) % NT == 0, "whole tasks per thread");
         C2<T> v[TPT][R0];
 #pragma unroll
@@ -1169,9 +1176,9 @@ k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __re
         const long long row = row0 + r;
         C2<T> a = mk<T>(0, 0), b = mk<T>(0, 0);
         if (row < nrows) {
-            const long long ro = ((long long)comp * nrows + row) * g.Hp;
-            a = *abin<MULTI>(g, A, ro, k);
-            b = *abin<MULTI>(g, A, ro, N - k);
+            const C2<T>* src = A + ((long long)comp * nrows + row) * g.Hp;
+            a = *abin<MULTI>(g, src, k);
+            b = *abin<MULTI>(g, src, N - k);
         }
         const C2<T> w = __ldg(tw_dense<T, 2 * N>(tw) + k);   // W_Px^k, used conjugated
         {
@@ -1520,10 +1527,10 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
         const long long row = row0 + col % ROWS;
         pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
         if (e < ITEMS && row < nrows) {
-            const long long ro = ((long long)(col / ROWS) * nrows + row) * g.Hp;
-            pa[it] = *abin<MULTI>(g, A, ro, k);
-            pb[it] = *abin<MULTI>(g, A, ro, N - k);
-            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, A, ro, N / 2);
+            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
+            pa[it] = *abin<MULTI>(g, src, k);
+            pb[it] = *abin<MULTI>(g, src, N - k);
+            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, src, N / 2);
         }
     }
     auto pre = [&](C2<T>* scol, int k, C2<T> a, C2<T> b) {
