@@ -15,8 +15,10 @@ Arms:
   python bench.py [--gpus N --steps K --warmup W]     this engine (libmagfd_b200.so)
   python bench.py --impl reference ...                 the reference CPU code (oracle/_ref)
 
-Multi-GPU (torchrun, N>1): round 1 runs one full replica per rank (weak
-scaling, no data-path collective); see DESIGN.md section "Multi-GPU".
+Multi-GPU (torchrun, N>1): the z-slab decomposition over NCCL (strong scaling
+of the one grid: each rank owns nz/N planes; two all-to-all transposes of the
+x-spectrum per step + a one-plane M halo); independent replicas only if the
+slab path cannot start.  See DESIGN.md section (e).
 """
 import argparse
 import ctypes as C
