@@ -46,6 +46,8 @@ constexpr bool kYZSmall = true;
 constexpr bool kK2Tma = true;
 // K4 input through a ring of TMA-staged half tiles (persistent CTAs).
 constexpr bool kK4Tma = true;
+// K3 with one y row per CTA (twice the CTAs per SM) instead of the pair {v, Py-v}.
+constexpr bool kK3SingleRow = true;
 constexpr long long kFuseK1MaxCells = 4LL << 20;
 // L2 prefetch (cp.async.bulk.prefetch) of the x passes' inputs one resident
 // wave of CTAs ahead, and of K5's epilogue rows while its FFT runs.
@@ -266,6 +268,7 @@ private:
     int k2_grid_ = 0, k2_box_ = 0;
     CUtensorMap tmA_{};                        // A as [3 nz ny] x [Hp] 8-byte elements
     bool k4_tma_ = false;                      // K4 with TMA-staged input (k_fft_y_inv_tma)
+    bool k3_srow_ = false;                     // K3 one y row per CTA (Z2Cfg SROW)
     int k4_grid_ = 0;
     CUtensorMap tmB_{};                        // B as [G 3 nz Py] x [Wb] 8-byte elements
     bool yz() const { return yz_small_ && stop_after_ == 0; }   // debug_stage needs the separate passes

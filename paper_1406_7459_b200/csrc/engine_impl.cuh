@@ -241,6 +241,8 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             if constexpr (z_variant<T, L>() == 2) {
                 set_smem<T>((const void*)k_fft_z_conv2<T, L, true>, Z2Cfg<T, L>::SMEM);
                 set_smem<T>((const void*)k_fft_z_conv2<T, L, false>, Z2Cfg<T, L>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, true, true>, Z2Cfg<T, L, true>::SMEM);
+                set_smem<T>((const void*)k_fft_z_conv2<T, L, false, true>, Z2Cfg<T, L, true>::SMEM);
             }
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
@@ -313,6 +315,9 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     if (const char* e = getenv("MFD_FUSE_K1"))   // A/B switch: 0 off, 2 on regardless of the grid size
         fuse_k1_ = atoi(e) == 2 ? (kFuseK1 && G == 1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0)
                                 : fuse_k1_ && atoi(e) != 0;
+    // Measured (single-row vs pair): f32 C4 0.609 -> 0.583 ms, C3 -12 %, C5 -14 %; f64 C4 1.18 -> 1.30 ms
+    k3_srow_ = kK3SingleRow && sizeof(T) == 4;
+    if (const char* e = getenv("MFD_K3_SROW")) k3_srow_ = atoi(e) != 0;   // A/B switch
     if (getenv("MFD_VERBOSE"))
         fprintf(stderr, "mfd: K2 tma %d grid %d | K4 tma %d grid %d | yz_small %d fuse_k1 %d\n", (int)k2_tma_,
                 k2_grid_, (int)k4_tma_, k4_grid_, (int)yz_small_, (int)fuse_k1_);
@@ -526,10 +531,17 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
             dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
             k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, B_, Kt_, ybuf_, ctl);
         } else if constexpr (z_variant<T, L>() == 2) {
-            using CF = Z2Cfg<T, L>;
-            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
-            auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true> : k_fft_z_conv2<T, L, false>;
-            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+            if (k3_srow_) {
+                using CF = Z2Cfg<T, L, true>;
+                dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Py_, 1);
+                auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true, true> : k_fft_z_conv2<T, L, false, true>;
+                k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+            } else {
+                using CF = Z2Cfg<T, L>;
+                dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
+                auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true> : k_fft_z_conv2<T, L, false>;
+                k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
+            }
         } else {
             using CF = ZCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);

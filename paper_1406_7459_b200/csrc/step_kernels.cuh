@@ -694,50 +694,49 @@ __device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* _
 // the tensor product and the transposed inverse stage 1 (same positions), so
 // the product costs no extra shared-memory round trip; the inverse stage 0
 // goes shared -> HBM keeping the nz planes.
-template <class T, int L> struct Z2Cfg {
+// SROW: one y row per CTA (the CTAs of rows v and Py-v are launched next to
+// each other, so the second one's tensor bins come from L2) instead of the
+// pair {v, Py-v}: half the shared memory and threads, twice the CTAs per SM.
+template <class T, int L, bool SROW = false> struct Z2Cfg {
     static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
     static constexpr int CS = sizeof(C2<T>);
-#ifdef MFD_K3W
-    static constexpr int W = MFD_K3W;
-#else
     static constexpr int W = (sizeof(T) == 4 ? 16 : 8) / (R1 >= 16 ? 2 : 1);
-#endif
-    static constexpr int NCOL = 6 * W;
-    static constexpr int NT = W * R1 * 2;
+    static constexpr int NROW = SROW ? 1 : 2;
+    static constexpr int NCOL = 3 * NROW * W;
+    static constexpr int NT = W * R1 * NROW;
     static constexpr int SMEM = NCOL * L * CS;
     // resident CTAs per SM the register budget is sized for (shared memory permitting)
     // tensor bins loaded one phase ahead (register budget: R1 <= 8 only)
     static constexpr bool KPRE = R1 <= 8;
-#ifdef MFD_K3MINB
-    static constexpr int MINB = MFD_K3MINB;
-#else
-    static constexpr int MINB = KPRE ? cmax(1, cmin(2, (200 * 1024) / SMEM)) : 1;
-#endif
+    static constexpr int MINB = KPRE ? cmax(1, cmin(2 * (3 - NROW), (200 * 1024) / SMEM)) : 1;
 };
 
 // FZ: nz == Pz/2, so the pruned first/last stages never meet a plane >= nz.
 // Padding x-bins (>= Hv, inside the block pitch) are computed, not masked.
-template <class T, int L, bool FZ>
-__global__ void __launch_bounds__(Z2Cfg<T, L>::NT, Z2Cfg<T, L>::MINB)
+template <class T, int L, bool FZ, bool SROW = false>
+__global__ void __launch_bounds__(Z2Cfg<T, L, SROW>::NT, Z2Cfg<T, L, SROW>::MINB)
 k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
               const int* __restrict__ ybuf, Ctl ctl) {
-    using CF = Z2Cfg<T, L>;
+    using CF = Z2Cfg<T, L, SROW>;
     constexpr int W = CF::W, NCOL = CF::NCOL, R0 = CF::R0, R1 = CF::R1;
+    constexpr int CO = CF::NROW * W;   // column stride of the components
     static_assert(Plan<T, L>::S == 2 && R0 % R1 == 0, "two-stage plans with R0 % R1 == 0 only");
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;               // x-bin within this rank's block
-    const int v = blockIdx.y;
     const int Py = g.Py, nz = g.nzg, Wb = g.Wb;
+    // SROW: y block b -> frequency pair v = (b+1)/2, row v (r = 0) or Py-v (r = 1)
+    const int v = SROW ? ((int)blockIdx.y + 1) / 2 : (int)blockIdx.y;
     const int vp = (Py - v) & (Py - 1);
     const bool pair = vp != v;
-    const int w = threadIdx.x % W, n2 = (threadIdx.x / W) % R1, r = threadIdx.x / (W * R1);
-    const bool live = pair || r == 0;
+    const int w = threadIdx.x % W, n2 = (threadIdx.x / W) % R1;
+    const int r = SROW ? (pair ? (int)(blockIdx.y & 1) : 0) : (int)threadIdx.x / (W * R1);
+    const bool live = SROW || pair || r == 0;
     const long long cstride = g.S_c;
-    C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + zoff(k)
-    // smem column of (comp c, row r, bin w): (c*2 + r)*W + w; layout [pos][NCOL]
-    C2<T>* scol = sm + r * W + w;
+    C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + k*S_k
+    // smem column of (comp c, row r, bin w): c*CO + r*W + w; layout [pos][NCOL]
+    C2<T>* scol = sm + (SROW ? 0 : r * W) + w;
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
     // Software pipeline over the three components: the loads of component
     // c+1 are in flight while component c is transformed.  (A persistent
@@ -766,7 +765,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int k = 1; k < R0; ++k) x[k] = cmul<T>(x[k], twr[k]);
 #pragma unroll
-        for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * 2 * W] = x[k];
+        for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * CO] = x[k];
     }
     }
     // ---- stage 1 + tensor product + inverse stage 1, in registers.  The
@@ -793,7 +792,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int q = 0; q < R1; ++q) y[c][q] = scol[(k0 * R1 + q) * NCOL + c * 2 * W];
+            for (int q = 0; q < R1; ++q) y[c][q] = scol[(k0 * R1 + q) * NCOL + c * CO];
 #pragma unroll
         for (int c = 0; c < 3; ++c) dft<T, R1, false>(y[c]);
         if (live) {
@@ -814,7 +813,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int q = 0; q < R1; ++q) scol[(k0 * R1 + q) * NCOL + c * 2 * W] = y[c][q];
+            for (int q = 0; q < R1; ++q) scol[(k0 * R1 + q) * NCOL + c * CO] = y[c][q];
     }
     __syncthreads();
     // ---- inverse stage 0 (transposed): gather k0*R1 + n2, conj twiddle, IDFT, keep z < nz
@@ -825,7 +824,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     for (int c = 0; c < 3; ++c) {
         C2<T> x[R0];
 #pragma unroll
-        for (int k = 0; k < R0; ++k) x[k] = scol[(k * R1 + n2) * NCOL + c * 2 * W];
+        for (int k = 0; k < R0; ++k) x[k] = scol[(k * R1 + n2) * NCOL + c * CO];
 #pragma unroll
         for (int k = 1; k < R0; ++k) x[k] = cmulc<T>(x[k], twr[k]);
         dft<T, R0, true, false, true>(x);
