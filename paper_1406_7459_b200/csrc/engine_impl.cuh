@@ -205,14 +205,14 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
                 k1_smem_ = sm_bytes;
             }
             set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM, false);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, LCfg<T, L>::SMEM, false);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::SMEM, false);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, true>, LCfg<T, L>::SMEM, false);
-            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, true>, LCfg<T, L>::SMEM, false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, k5_smem<T, L, 0, false>(), false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, k5_smem<T, L, 0, false>(), false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, true>, k5_smem<T, L, 0, true>(), false);
+            set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, true>, k5_smem<T, L, 0, true>(), false);
             if (G > 1) {
                 set_smem<T>((const void*)k_c2r_x_llg<T, L, true>, LCfg<T, L>::SMEM, false);
-                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, false, true>, LCfg<T, L>::SMEM, false);
-                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, false, true>, LCfg<T, L>::SMEM, false);
+                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true, 0, false, true>, k5_smem<T, L, 0, false>(), false);
+                set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false, 0, false, true>, k5_smem<T, L, 0, false>(), false);
             }
             k5_blocks_ = (nrows + LCfg<T, L>::ROWS - 1) / LCfg<T, L>::ROWS;
             // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
@@ -225,7 +225,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_r2c_x<T, L>, XCfg<T, L>::NT,
                                                              XCfg<T, L>::SMEM), "occupancy");
             ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per5, k_c2r_x_llg_v<T, L, false>, LCfg<T, L>::NT,
-                                                             LCfg<T, L>::SMEM), "occupancy");
+                                                             k5_smem<T, L, 0, false>()), "occupancy");
             geo_.pf1 = per1 * nsm;
             geo_.pf5 = per5 * nsm;
             geo_.pfm = small_x_ ? 0 : kL2PrefetchMask;
@@ -599,7 +599,8 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
                                        : k_c2r_x_llg_v<T, L, false, 0, false, true>)
                     : io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 0, true> : k_c2r_x_llg_v<T, L, true, 0, false>)
                               : (fwd ? k_c2r_x_llg_v<T, L, false, 0, true> : k_c2r_x_llg_v<T, L, false, 0, false>);
-            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
+            const int smem = fwd && !multi ? k5_smem<T, L, 0, true>() : k5_smem<T, L, 0, false>();
+            k<<<grid, CF::NT, smem, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
         } else {
             auto* k = multi ? k_c2r_x_llg<T, L, true> : k_c2r_x_llg<T, L, false>;
             k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);

@@ -38,15 +38,48 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
     static constexpr int NT = RS > 0 ? clampNT(ROWS * N / E) : clampNT(cmax(128, ROWS * N / E));
     static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
 };
+#ifndef MFD_K5_STAGE
+#define MFD_K5_STAGE 0   // measured slower at C4 (2 CTAs/SM): 0.372 -> 0.455 ms
+#endif
+#ifndef MFD_Y_TILE_MAX
+// bytes of the K2/K4 shared tile (W columns x L).  64 KB keeps 2+ CTAs/SM;
+// the three-stage Py = 2048 pass (C5) is faster with 128 KB tiles, i.e.
+// 64-byte (f32) column groups at 1 CTA/SM: K2 3.72 -> 2.90 ms, K4 4.08 -> 2.76 ms
+#define MFD_Y_TILE_MAX(L) ((L) >= 2048 ? 131072 : 65536)
+#endif
+#ifndef MFD_Z2_W
+#define MFD_Z2_W 0             // K3 (two-stage) columns per CTA override (0: default)
+#endif
+#ifndef MFD_K5_STG_MINB
+#define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
+#endif
+#ifndef MFD_K5_STAGE_MAX
+#define MFD_K5_STAGE_MAX 113   // KB of shared memory per CTA the staged K5 may use
+#endif
 template <class T, int N, int RS = 0> struct LCfg {   // K5
     static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(32, 2048 / cmax(N, 1)));
     static constexpr int NT = RS > 0 ? 64 : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
-    static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM)) : 1;
+    // STG: the CTA's M rows and their two in-plane y-neighbour rows are
+    // staged into shared memory by cp.async at kernel start, so their L2
+    // latency overlaps the inverse x FFT; the epilogue then reads M, its x
+    // and y neighbours from shared memory and only the z rows from L2.
+    static constexpr int SROWS = ROWS + 2;
+    static constexpr int SOFF = (SMEM + 15) / 16 * 16;   // 16-byte aligned staging offset
+    static constexpr bool STG = MFD_K5_STAGE && sizeof(T) == 4 && RS == 0 && ROWS >= 4 &&
+                                SOFF + 3 * SROWS * N * (int)sizeof(T) <= MFD_K5_STAGE_MAX * 1024;
+    static constexpr int MINB = sizeof(T) == 4 ? (STG && MFD_K5_STG_MINB > 0 ? MFD_K5_STG_MINB
+                                                                         : cmax(1, cmin(3, (200 * 1024) / SMEM)))
+                                               : 1;
+    static constexpr int SMEM_STG = STG ? SOFF + 3 * SROWS * N * (int)sizeof(T) : SMEM;
 };
+// dynamic shared memory of a K5 variant (the fused-K1 variant does not stage M)
+template <class T, int N, int RS, bool FWD> constexpr int k5_smem() {
+    return FWD ? LCfg<T, N, RS>::SMEM : LCfg<T, N, RS>::SMEM_STG;
+}
 template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int CS = sizeof(C2<T>);
-    static constexpr int W = cmax(1, cmin(128 / CS, 65536 / (L * CS)));   // <= 64 KB tile: 2+ CTAs/SM
+    static constexpr int W = cmax(1, cmin(128 / CS, MFD_Y_TILE_MAX(L) / (L * CS)));   // <= 64 KB tile: 2+ CTAs/SM
     static constexpr int NT = clampNT(W * L / regE<T>());
     static constexpr int SMEM = Plan<T, L>::S >= 2 ? W * L * CS : 0;
     // resident CTAs per SM the register budget is sized for (shared memory permitting)
@@ -700,7 +733,8 @@ __device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* _
 template <class T, int L, bool SROW = false> struct Z2Cfg {
     static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
     static constexpr int CS = sizeof(C2<T>);
-    static constexpr int W = (sizeof(T) == 4 ? 16 : 8) / (R1 >= 16 ? 2 : 1);
+    // f32: 16 columns (128-byte rows) also at R1 = 16 (Pz = 256, C5: 7.68 -> 7.07 ms)
+    static constexpr int W = MFD_Z2_W > 0 && sizeof(T) == 4 ? MFD_Z2_W : sizeof(T) == 4 ? 16 : 8 / (R1 >= 16 ? 2 : 1);
     static constexpr int NROW = SROW ? 1 : 2;
     static constexpr int NCOL = 3 * NROW * W;
     static constexpr int NT = W * R1 * NROW;
@@ -1330,6 +1364,13 @@ __device__ __forceinline__ void vload(const T* p, T* out) {
     else { out[0] = v.x; out[1] = v.y; }
 }
 template <class T>
+__device__ __forceinline__ void vlds(const T* p, T* out) {   // shared-memory 16-byte vector
+    using VT = typename V16<T>::type;
+    const VT v = *reinterpret_cast<const VT*>(p);
+    if constexpr (V16<T>::V == 4) { out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w; }
+    else { out[0] = v.x; out[1] = v.y; }
+}
+template <class T>
 __device__ __forceinline__ void vstore(T* p, const T* in) {
     using VT = typename V16<T>::type;
     VT v;
@@ -1346,12 +1387,16 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // accumulated in the reference order x-, x+, y-, y+, z-, z+ (fields.hpp:33-48).
 // fsm (fused next-step x pass): the new M of the V cells also goes to shared
 // memory as (x[2n], x[2n+1]) pairs at component stride fstride.
-template <class T, bool SUMS>
+// STG: ms = the staged copy of this row (component 0, x = 0) in shared
+// memory, component stride mcs, row pitch mpitch (rows j-1 and j+1 of the
+// same plane are the adjacent staged rows).
+template <class T, bool SUMS, bool STG = false>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                           const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
                                           const Halo<T>& hl, long long c0, int i0, int j, int k,
                                           const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
-                                          C2<T>* fsm = nullptr, int fstride = 0) {
+                                          C2<T>* fsm = nullptr, int fstride = 0,
+                                          const T* ms = nullptr, int mcs = 0, int mpitch = 0) {
     constexpr int V = V16<T>::V;
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
     const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
@@ -1365,19 +1410,25 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const T* p = M + c * n + c0;
-        vload<T>(p, m[c]);
+        const T* sp = STG ? ms + c * mcs + i0 : nullptr;
+        if (STG) vlds<T>(sp, m[c]); else vload<T>(p, m[c]);
         if (!P.exch) {
 #pragma unroll
             for (int q = 0; q < V; ++q) H[c][q] = hd[c][q];
             continue;
         }
         T ym[V], yp[V], zm[V], zp[V];
-        if (hy0) vload<T>(p - sy, ym);
-        if (hy1) vload<T>(p + sy, yp);
         if (hz0) vload<T>(k > 0 ? p - sz : hl.lo + c * sz + inplane, zm);          // slab edge: halo plane
         if (hz1) vload<T>(k < g.nz - 1 ? p + sz : hl.hi + c * sz + inplane, zp);
-        const T xl = hx0 ? __ldg(p - 1) : T(0);
-        const T xr = hx1 ? __ldg(p + V) : T(0);
+        if (STG) {
+            if (hy0) vlds<T>(sp - mpitch, ym);
+            if (hy1) vlds<T>(sp + mpitch, yp);
+        } else {
+            if (hy0) vload<T>(p - sy, ym);
+            if (hy1) vload<T>(p + sy, yp);
+        }
+        const T xl = hx0 ? (STG ? sp[-1] : __ldg(p - 1)) : T(0);
+        const T xr = hx1 ? (STG ? sp[V] : __ldg(p + V)) : T(0);
 #pragma unroll
         for (int q = 0; q < V; ++q) {
             const T mc = m[c][q];
@@ -1490,6 +1541,22 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const long long nrows = (long long)g.ny * g.nz;
     const long long row0 = (long long)blockIdx.x * ROWS;
+    constexpr bool STG = CF::STG && !FWD;
+    constexpr int SROWS = CF::SROWS;
+    T* ms = reinterpret_cast<T*>(smem_raw + CF::SOFF);   // [3][SROWS][N]: rows row0-1 .. row0+ROWS
+    if constexpr (STG) {
+        constexpr int NV = N / V, NCH = 3 * SROWS * NV;   // 16-byte chunks (nx <= N)
+        const int nv = g.nx / V;
+#pragma unroll
+        for (int q0 = 0; q0 < NCH; q0 += NT) {
+            const int q = q0 + threadIdx.x;
+            const int c = q / (SROWS * NV), rr = (q / NV) % SROWS, v = q % NV;
+            const long long row = row0 - 1 + rr;
+            if ((NCH % NT == 0 || q < NCH) && v < nv && row >= 0 && row < nrows)
+                cp_async16(ms + (c * SROWS + rr) * N + v * V, M + c * g.ncell + row * g.nx + v * V);
+        }
+        cp_commit();
+    }
     if ((g.pfm & 6) && threadIdx.x < 3) {
         // this CTA's M rows with their y / z neighbour rows (read by the
         // epilogue, after the inverse FFT) ...
@@ -1561,6 +1628,10 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
         fft_inverse<T, N, NCOL, NT, false, true, true, true, true>(lds, lds, sts, sts, tw);
         __syncthreads();
     }
+    if constexpr (STG) {
+        cp_wait<0>();
+        __syncthreads();
+    }
     double tmax = 0;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
     int bad = 0;
@@ -1583,8 +1654,8 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
                 hd[c][q] = z.x * scale;
                 hd[c][q + 1] = z.y * scale;
             }
-        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
-                           FWD ? sm + r * LP : nullptr, ROWS * LP);
+        cells_vec<T, SUMS, STG>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
+                                FWD ? sm + r * LP : nullptr, ROWS * LP, ms + (r + 1) * N, SROWS * N, N);
     }
     if constexpr (FWD && N >= 2) {
         // next step's K1 on the rows in shared memory (pairs beyond nx/2 are padding)
