@@ -68,6 +68,13 @@ __global__ void k_vortex(T* m, int nx, int ny, int nz, int nzg, int k0, double d
     m[c + 2 * n] = static_cast<T>(__dmul_rn(Ms, mz));
 }
 
+// Largest x length with the 1-2-row K1/K5 variants for few-row grids (SP4
+// 128x32x1: N = 128; SP4 refined 512x128x4: N = 512, 512 rows).
+#ifndef MFD_SMALL_X_MAX
+#define MFD_SMALL_X_MAX 512
+#endif
+constexpr int kSmallXMax = MFD_SMALL_X_MAX;
+
 template <class T>
 static void set_smem(const void* fn, int bytes, bool carve = true) {
     if (bytes > 48 * 1024)
@@ -218,7 +225,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             // small grids (e.g. SP4, 32 rows): 1-2 rows per CTA so the x passes use the SMs
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
-            small_x_ = L >= 2 && L <= 256 && k5_blocks_ < 2 * nsm && g.nx % V16<T>::V == 0;
+            small_x_ = L >= 2 && L <= kSmallXMax && k5_blocks_ < 2 * nsm && g.nx % V16<T>::V == 0;
             if (small_x_) k5_blocks_ = nrows;
             // L2 prefetch distances: one resident wave of CTAs
             int per1 = 0, per5 = 0;
@@ -474,7 +481,7 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
             if constexpr (L >= 2)
                 k_r2c_x_pipe<T, L><<<k1_grid_, CF::NT, k1_smem_, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
         } else if (small_x_) {
-            if constexpr (L >= 2 && L <= 256) {
+            if constexpr (L >= 2 && L <= kSmallXMax) {
                 using CS = XCfg<T, L, 2>;
                 dim3 grid((unsigned)((nrows + 1) / 2), 3);
                 auto* k = geo_.G > 1 ? k_r2c_x<T, L, 2, true> : k_r2c_x<T, L, 2, false>;
@@ -581,7 +588,7 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     with_pow2(geo_.N, [&]<int L>() {
         using CF = LCfg<T, L>;
         dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 1);
-        if constexpr (L >= 2 && L <= 256) {
+        if constexpr (L >= 2 && L <= kSmallXMax) {
             if (small_x_) {   // one row per CTA (few-row grids such as SP4)
                 using CS = LCfg<T, L, 1>;
                 auto* k = geo_.G > 1
