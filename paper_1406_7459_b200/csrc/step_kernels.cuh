@@ -53,6 +53,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K5_STG_MINB
 #define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
 #endif
+#ifndef MFD_K5_F64_MINB
+#define MFD_K5_F64_MINB 2   // f64 K5: 128 registers, 2 CTAs/SM (C4 f64 K5 1.196 -> 0.949 ms despite a 144-byte spill)
+#endif
 #ifndef MFD_K5_STAGE_MAX
 #define MFD_K5_STAGE_MAX 113   // KB of shared memory per CTA the staged K5 may use
 #endif
@@ -70,7 +73,7 @@ template <class T, int N, int RS = 0> struct LCfg {   // K5
                                 SOFF + 3 * SROWS * N * (int)sizeof(T) <= MFD_K5_STAGE_MAX * 1024;
     static constexpr int MINB = sizeof(T) == 4 ? (STG && MFD_K5_STG_MINB > 0 ? MFD_K5_STG_MINB
                                                                          : cmax(1, cmin(3, (200 * 1024) / SMEM)))
-                                               : 1;
+                                               : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
     static constexpr int SMEM_STG = STG ? SOFF + 3 * SROWS * N * (int)sizeof(T) : SMEM;
 };
 // dynamic shared memory of a K5 variant (the fused-K1 variant does not stage M)
