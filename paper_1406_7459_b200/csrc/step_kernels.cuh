@@ -53,6 +53,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K5_STG_MINB
 #define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
 #endif
+#ifndef MFD_YINV_F64_MINB
+#define MFD_YINV_F64_MINB 2   // f64 K4 (non-TMA y inverse): resident CTAs/SM its register budget assumes
+#endif
 #ifndef MFD_K5_F64_MINB
 #define MFD_K5_F64_MINB 2   // f64 K5: 128 registers, 2 CTAs/SM (C4 f64 K5 1.196 -> 0.949 ms despite a 144-byte spill)
 #endif
@@ -87,6 +90,8 @@ template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int SMEM = Plan<T, L>::S >= 2 ? W * L * CS : 0;
     // resident CTAs per SM the register budget is sized for (shared memory permitting)
     static constexpr int MINB = cmax(1, cmin(3, SMEM > 0 ? (200 * 1024) / SMEM : 3));
+    // K4 in f64: at 3 CTAs/SM (80 registers) the inverse spills 456 bytes per thread
+    static constexpr int MINB_INV = sizeof(T) == 8 && MFD_YINV_F64_MINB > 0 ? cmin(MINB, MFD_YINV_F64_MINB) : MINB;
 };
 template <class T, int L> struct ZCfg {   // K3
     static constexpr int CS = sizeof(C2<T>);
@@ -473,7 +478,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
 
 // ------------------------------------------------------------------ K4
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB)
+__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB_INV)
 k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
