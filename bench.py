@@ -188,19 +188,21 @@ def run_reference_arm(args, ws, rank):
     g = WORKLOADS[args.workload][0]
     sample = cpu_sample_grid(g)
     try:
-        v, ms, setup, done = cpu_reference(args.steps, args.warmup, threads, sample, 32)
+        v, ms, setup, done = cpu_reference(args.steps, args.warmup, threads, sample, args.precision)
     except Exception as e:  # reference not built on this box
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return
-    desc = (f"reference Simulation<float>::step (oracle/_ref, built from /root/reference/proj) on "
+    ct = "float" if args.precision == 32 else "double"
+    dt = "f32" if args.precision == 32 else "f64"
+    desc = (f"reference Simulation<{ct}>::step (oracle/_ref, built from /root/reference/proj) on "
             f"{sample[0]}x{sample[1]}x{sample[2]} cells (bounded sample of {g[0]}x{g[1]}x{g[2]}; same "
             f"material, cell size, terms); {args.warmup} warm-up + median of {done} steps; setup {setup:.1f}s excluded")
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
-                   "sample_grid": list(sample[:3]), "precision": "f32", "parallelism": "host threads"},
+                   "sample_grid": list(sample[:3]), "precision": dt, "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -318,7 +320,7 @@ def run_ours(args, ws, rank, local):
             sample = cpu_sample_grid(g)
             v, cms, setup, done = cpu_reference(3, 1, threads, sample, prec, budget_s=25)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"reference Simulation<float>::step (oracle/_ref) on {sample[0]}x{sample[1]}x{sample[2]} "
+                   "sample": f"reference Simulation<{'float' if prec == 32 else 'double'}>::step (oracle/_ref) on {sample[0]}x{sample[1]}x{sample[2]} "
                              f"cells, same material/cell size/terms, {threads} host threads, 1 warm-up + median of "
                              f"{done} steps ({cms:.0f} ms/step), setup {setup:.1f}s excluded"}
         except Exception as e:
