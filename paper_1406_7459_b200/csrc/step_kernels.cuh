@@ -53,6 +53,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K5_STG_MINB
 #define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
 #endif
+#ifndef MFD_YFWD_F64_MINB
+#define MFD_YFWD_F64_MINB 2   // f64 K2 (non-TMA y forward): 128 registers, 2 CTAs/SM (C4 f64 K2 0.713 -> 0.631 ms)
+#endif
 #ifndef MFD_YINV_F64_MINB
 #define MFD_YINV_F64_MINB 2   // f64 K4 (non-TMA y inverse): resident CTAs/SM its register budget assumes
 #endif
@@ -92,6 +95,7 @@ template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int MINB = cmax(1, cmin(3, SMEM > 0 ? (200 * 1024) / SMEM : 3));
     // K4 in f64: at 3 CTAs/SM (80 registers) the inverse spills 456 bytes per thread
     static constexpr int MINB_INV = sizeof(T) == 8 && MFD_YINV_F64_MINB > 0 ? cmin(MINB, MFD_YINV_F64_MINB) : MINB;
+    static constexpr int MINB_FWD = sizeof(T) == 8 && MFD_YFWD_F64_MINB > 0 ? cmin(MINB, MFD_YFWD_F64_MINB) : MINB;
 };
 template <class T, int L> struct ZCfg {   // K3
     static constexpr int CS = sizeof(C2<T>);
@@ -381,7 +385,7 @@ k_r2c_x_pipe(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>*
 // of being masked per element.  FY: ny == Py/2 (power-of-two ny), so the
 // pruned first stage never meets a row >= ny and the row test disappears.
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB)
+__global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB_FWD)
 k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
