@@ -17,8 +17,12 @@ Arms:
 
 Multi-GPU (torchrun, N>1): the z-slab decomposition over NCCL (strong scaling
 of the one grid: each rank owns nz/N planes; two all-to-all transposes of the
-x-spectrum per step + a one-plane M halo); independent replicas only if the
-slab path cannot start.  See DESIGN.md section (e).
+x-spectrum per step + a one-plane M halo).  If the slab path cannot start on
+any rank, every rank fails (no silent fallback).  See DESIGN.md section (e).
+
+Both arms print the same `config` object (the grid the step runs on); the CPU
+legs run the reference on the full grid with all host threads, plus a 1-thread
+row.
 """
 import argparse
 import ctypes as C
@@ -155,56 +159,85 @@ def allmax(ws, v):
 
 
 # --------------------------------------------------------------- CPU reference
-def cpu_reference(steps, warmup, threads, sample_grid, precision=32, budget_s=None):
+def cpu_reference(steps, warmup, threads, grid, precision=32, budget_s=None, one_thread_steps=0):
     """Reference Simulation<T>::step (oracle/_ref, the unmodified reference code) on
-    the host cores.  Returns (cell-updates/s, ms/step, setup_s, steps_done)."""
+    the host cores: setup on `threads` threads (timed separately), `warmup` steps,
+    then the median of `steps` per-step wall times (the reference bench protocol,
+    cli.cpp:95-117), stopping early once `budget_s` of stepping is spent.  With
+    one_thread_steps > 0 the same state then steps on a 1-thread backend.
+    Returns dict(value, ms, setup_s, steps, ms_1thread, steps_1thread)."""
     from oracle import oracle as O
     if not O.ref_available():
         raise RuntimeError("oracle/_ref/libmagfd_ref.so not built")
-    g = sample_grid
-    spec = O.Spec(*g, **MATERIAL, h_ext=H_EXT, dt=DT, parallel=True, threads=threads)
+    import numpy as np
+    spec = O.Spec(*grid, **MATERIAL, h_ext=H_EXT, dt=DT, parallel=True, threads=threads)
     t0 = time.perf_counter()
     r = O.Ref(spec, precision)
     n = spec.n
-    u = 1 / 3 ** 0.5
-    r.set_m(__import__("numpy").full((3, n), 8e5 * u))
+    r.set_m(np.full((3, n), 8e5 / 3 ** 0.5))
     setup = time.perf_counter() - t0
+
+    def timed(k, budget):
+        times = []
+        for _ in range(k):
+            t1 = time.perf_counter()
+            r.step(1)
+            times.append(time.perf_counter() - t1)
+            if budget and sum(times) > budget:
+                break
+        return times
+
     r.step(warmup)
-    times = []
-    for _ in range(steps):
-        t1 = time.perf_counter()
-        r.step(1)
-        times.append(time.perf_counter() - t1)
-        if budget_s and sum(times) > budget_s:
-            break
+    times = timed(steps, budget_s)
     ms = statistics.median(times) * 1e3
-    return n / (ms / 1e3), ms, setup, len(times)
+    out = {"value": n / (ms / 1e3), "ms": ms, "setup_s": setup, "steps": len(times),
+           "ms_1thread": None, "steps_1thread": 0}
+    if one_thread_steps > 0:
+        r.set_step_threads(1)
+        t1 = timed(one_thread_steps, None)
+        out["ms_1thread"] = statistics.median(t1) * 1e3
+        out["steps_1thread"] = len(t1)
+    return out
+
+
+def config_of(workload, prec):
+    """The `config` object both arms print (identical for the same grid / precision)."""
+    g = WORKLOADS[workload][0]
+    dt = "f32" if prec == 32 else "f64"
+    return {"workload": WORKLOADS[workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
+            "precision": dt, "terms": "demag+exchange+anisotropy+zeeman",
+            "material": "Ms 8e5, A 1.3e-11, Ku 4e4 (z), H_ext (1e4,0,0) A/m, alpha 0.02, dt 1e-14 s"}
 
 
 def run_reference_arm(args, ws, rank):
+    """The reference's own CPU implementation on the same grid as our arm (the full
+    BASELINE grid, all host threads).  A step takes seconds at the film sizes, so
+    the warm-up is capped at 3 steps (the reference bench's own count,
+    cli.cpp:95-99) and the timed steps stop after a 150 s budget."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     g = WORKLOADS[args.workload][0]
-    sample = cpu_sample_grid(g)
+    warm = min(args.warmup, 3)
     try:
-        v, ms, setup, done = cpu_reference(args.steps, args.warmup, threads, sample, args.precision)
+        r = cpu_reference(args.steps, warm, threads, g, args.precision, budget_s=150)
     except Exception as e:  # reference not built on this box
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return
     ct = "float" if args.precision == 32 else "double"
     dt = "f32" if args.precision == 32 else "f64"
-    desc = (f"reference Simulation<{ct}>::step (oracle/_ref, built from /root/reference/proj) on "
-            f"{sample[0]}x{sample[1]}x{sample[2]} cells (bounded sample of {g[0]}x{g[1]}x{g[2]}; same "
-            f"material, cell size, terms); {args.warmup} warm-up + median of {done} steps; setup {setup:.1f}s excluded")
+    desc = (f"reference Simulation<{ct}>::step (oracle/_ref, built from /root/reference/proj with its "
+            f"Release flags) on the full {g[0]}x{g[1]}x{g[2]} grid, {threads} host threads; {warm} warm-up + "
+            f"median of {r['steps']} steps; setup {r['setup_s']:.1f}s excluded")
     out = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": done, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
-                   "sample_grid": list(sample[:3]), "precision": dt, "parallelism": "host threads"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": desc},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": r["steps"], "warmup": warm, "ms_per_step": r["ms"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic (uniform (1,1,1)/sqrt3 start)",
+        "config": config_of(args.workload, args.precision),
+        "execution": f"CPU, {threads} host threads (reference Backend parallel)",
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference", "sample": desc,
+                         "setup_s": r["setup_s"]},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
 
@@ -231,31 +264,38 @@ def run_ours(args, ws, rank, local):
     s = 4 if prec == 32 else 8
     grid = E.Grid(*g)
     mk = dict(precision=prec, device=local, init_direction=(3 ** -0.5,) * 3)
-    mode, note = "1 GPU", None
+    mode = "1 GPU"
     if ws > 1:
-        # z-slab decomposition over NCCL (strong scaling of one grid); falls back to
-        # independent replicas (weak scaling) only if the slab path cannot start.
+        # z-slab decomposition over NCCL (strong scaling of one grid).  Every rank
+        # learns whether all ranks started; any failure stops all of them.
         import torch.distributed as dist
         box = [E.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
+        sim, err = None, None
         try:
             sim = E.Simulation(grid, E.Material(**MATERIAL), E.FieldConfig(True, True, True, True, H_EXT),
                                E.StepperConfig(dt=DT), world=ws, rank=rank, nccl_id=box[0], **mk)
-            mode = f"z-slab x{ws} (NCCL all-to-all + halo over NVLink)"
         except Exception as e:   # pragma: no cover - multi-GPU only
-            note = f"nccl slab path failed ({e}); replicas"
-            mode = "replica per GPU"
-    if ws == 1 or mode == "replica per GPU":
+            err = e
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"z-slab engine failed to start on rank {rank}: {err}" if err else
+                               "z-slab engine failed to start on another rank")
+        mode = f"z-slab x{ws} (NCCL all-to-all + halo over NVLink)"
+    else:
         sim = E.Simulation(grid, E.Material(**MATERIAL), E.FieldConfig(True, True, True, True, H_EXT),
                            E.StepperConfig(dt=DT), **mk)
     stream = torch.cuda.ExternalStream(sim.stream_handle(), device=torch.device("cuda", local))
     ncell = grid.cell_count                       # global cells of the grid
     slab_cells = sim.n                            # cells this rank owns
-    replicas = ws if mode == "replica per GPU" else 1
+    replicas = 1
 
-    # warm-up (graph capture + clocks ramp)
+    # warm-up (graph capture + clocks ramp), then capture the timed run's graphs
+    # so no capture / instantiation falls inside the timed region
     sim.step_async(args.warmup)
     sim.sync()
+    launches = sim.prepare_async(args.steps)   # kernel nodes of the timed graphs
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -297,6 +337,8 @@ def run_ours(args, ws, rank, local):
     host = torch.empty((3, slab_cells), dtype=torch.float32 if prec == 32 else torch.float64).pin_memory()
     host_np = host.numpy()
     host_np[:] = sim.get_m(dtype=np.float32 if prec == 32 else np.float64)
+    sim.set_m(host_np)
+    sim.step(1)            # captures the 1-step graph outside the timed loop
     barrier(ws)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -308,21 +350,28 @@ def run_ours(args, ws, rank, local):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(args.workload, {}).get(top)
+        try:   # per launch, keyed by workload and precision (one ncu --set full capture each)
+            traffic = json.load(open(tp)).get(args.workload, {}).get("f32" if prec == 32 else "f64", {}).get(top)
         except Exception:
             traffic = None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.skip_cpu:
+        ct = "float" if prec == 32 else "double"
         try:
             threads = os.cpu_count() or 1
-            sample = cpu_sample_grid(g)
-            v, cms, setup, done = cpu_reference(3, 1, threads, sample, prec, budget_s=25)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"reference Simulation<{'float' if prec == 32 else 'double'}>::step (oracle/_ref) on {sample[0]}x{sample[1]}x{sample[2]} "
-                             f"cells, same material/cell size/terms, {threads} host threads, 1 warm-up + median of "
-                             f"{done} steps ({cms:.0f} ms/step), setup {setup:.1f}s excluded"}
+            r = cpu_reference(3, 1, threads, g, prec, budget_s=60, one_thread_steps=1)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"reference Simulation<{ct}>::step (oracle/_ref) on the full {g[0]}x{g[1]}x{g[2]} grid, "
+                             f"same material/cell size/terms, {threads} host threads: 1 warm-up + median of "
+                             f"{r['steps']} steps ({r['ms']:.0f} ms/step); setup {r['setup_s']:.1f}s excluded",
+                   "ms_per_step": r["ms"], "setup_s": r["setup_s"],
+                   "one_thread": {"value": ncell / (r["ms_1thread"] / 1e3), "ms_per_step": r["ms_1thread"],
+                                  "cores": 1, "steps": r["steps_1thread"]}}
+            if args.workload == "film512":   # round-1 comparison point, kept as an extra field
+                s2 = cpu_sample_grid(g)
+                r2 = cpu_reference(3, 1, threads, s2, prec, budget_s=10)
+                cpu["sample_128x128x64"] = {"value": r2["value"], "ms_per_step": r2["ms"], "grid": list(s2[:3])}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -331,14 +380,15 @@ def run_ours(args, ws, rank, local):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak" if (ws == 1 or replicas > 1) else "strong", "vs_baseline": None,
+            "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None,
             "dtype": "f32" if prec == 32 else "f64",
-            "data": "synthetic (uniform (1,1,1)/sqrt3 start; random-free)",
-            "config": {"workload": WORKLOADS[args.workload][1], "grid": list(g[:3]), "cell_m": list(g[3:]),
-                       "precision": "f32" if prec == 32 else "f64", "terms": "demag+exchange+anisotropy+zeeman",
-                       "parallelism": mode, **({"note": note} if note else {}),
-                       "l2": "working set > 126 MB L2 (no flush needed)" if step_bytes > 4e8 else
-                             "working set fits L2 (inputs not flushed)"},
+            "data": "synthetic (uniform (1,1,1)/sqrt3 start)",
+            "config": config_of(args.workload, prec),
+            "execution": mode,
+            "l2": "working set > 126 MB L2 (no flush needed)" if step_bytes > 4e8 else
+                  "working set fits L2 (inputs not flushed)",
+            "timed_region": "graphs captured before the timed region (prepare_async); per-pass times from "
+                            "event-record nodes of a captured one-step graph",
             "steps_per_s": 1e3 / ms_step,
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -350,7 +400,7 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * slab_cells * s, "d2h_bytes_per_step": 8,
                     "how": "per step: Simulation.set_m from pinned host M (C ABI mfd_set_m) + Simulation.step "
                            "(mfd_step, returns the torque to the host)"},
-            "gpu_launches": sim.launches_per_step() * args.steps,
+            "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(out))

@@ -160,6 +160,10 @@ mfd_status mfd_debug_stage_f64(mfd_ctx* ctx, int stage, double* out);
 mfd_status mfd_device_state(mfd_ctx* ctx, void** m, long long* ncell, int* precision_bits);
 /* Run nsteps via CUDA graph on the context stream without host sync; pair with mfd_sync. */
 mfd_status mfd_step_async(mfd_ctx* ctx, long nsteps);
+/* Capture (without running) the CUDA graphs the next mfd_step_async(ctx, nsteps) will
+ * launch, so a timed region contains no capture / instantiation; *launches (may be
+ * NULL) = the kernel launches those graphs contain. */
+mfd_status mfd_prepare_async(mfd_ctx* ctx, long nsteps, long* launches);
 mfd_status mfd_sync(mfd_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* mfd_stream(mfd_ctx* ctx);
@@ -167,6 +171,10 @@ void* mfd_stream(mfd_ctx* ctx);
 int mfd_launches_per_step(const mfd_ctx* ctx);
 /* Algorithmic HBM bytes per step of the 5-pass model. */
 double mfd_model_bytes_per_step(const mfd_ctx* ctx);
+/* Kernel template instantiations this context has enqueued since creation, one per
+ * line ("K5 k_c2r_x_llg_v<f32,256,SUMS=0,RS=0,FWD=1,MULTI=0>", ...).  Copies at most
+ * len-1 bytes + NUL into buf (may be NULL) and returns the full length + 1. */
+int mfd_debug_variants(const mfd_ctx* ctx, char* buf, int len);
 
 #ifdef __cplusplus
 }

@@ -204,6 +204,11 @@ class Ref(_Sim):
             msg = self.lib.ref_last_error().decode()
             raise {1: ValueError, 2: RuntimeError, 3: LookupError}.get(rc, RuntimeError)(msg)
 
+    def set_step_threads(self, threads: int):
+        """Run the per-step calls on a `threads`-thread backend (setup stays on the
+        creation backend; <= 0 restores it)."""
+        self._call("set_step_threads", C.c_int(threads))
+
     def relax(self, cap: int = 100000):
         buf = (RefSample * cap)()
         n = C.c_long()

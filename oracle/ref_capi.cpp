@@ -82,6 +82,7 @@ struct Base {
     virtual void time(double* t, long* step) const = 0;
     virtual void setTime(double t, long step) = 0;
     virtual void energies(double out[5]) = 0;
+    virtual void setStepThreads(int threads) = 0;
 };
 
 template <class T>
@@ -93,6 +94,12 @@ struct Handle final : Base {
     fields::EffectiveFieldProvider<T> provider;
     SimState<T> state;
     VectorField<T> heffF, rhs;
+    // Backend the per-step calls use.  Simulation<T> takes its backend by
+    // pointer (sim.hpp:20,70) and every hot-path call receives it per call
+    // (fields.hpp:220, demag.hpp:194), so the setup can run on all threads and
+    // the steps on another pool (the CPU baseline's 1-thread row).
+    std::unique_ptr<Backend> alt;
+    const Backend* sb = &backend;
 
     Handle(const ref_spec& s, Grid g, MaterialParams m, fields::FieldConfig fc)
         : backend(s.parallel ? BackendKind::parallel : BackendKind::serial,
@@ -122,15 +129,15 @@ struct Handle final : Base {
     }
     // Same sequence as Simulation<T>::step (sim.hpp:33-42).
     double step() override {
-        provider.compute(state.M, heffF, backend, nullptr);
-        dynamics::llgRhs(state.M, heffF, mat, backend, rhs);
-        const double torque = dynamics::maxTorqueRate(rhs, mat.Ms, backend);
+        provider.compute(state.M, heffF, *sb, nullptr);
+        dynamics::llgRhs(state.M, heffF, mat, *sb, rhs);
+        const double torque = dynamics::maxTorqueRate(rhs, mat.Ms, *sb);
         const bool renorm = (state.step + 1) % stepper.renormalizeEvery == 0;
-        dynamics::eulerUpdate(state, rhs, stepper.dt, mat.Ms, renorm, backend);
+        dynamics::eulerUpdate(state, rhs, stepper.dt, mat.Ms, renorm, *sb);
         return torque;
     }
     void heff(double* x, double* y, double* z) override {
-        provider.compute(state.M, heffF, backend, nullptr);
+        provider.compute(state.M, heffF, *sb, nullptr);
         for (std::size_t c = 0; c < heffF.size(); ++c) {
             x[c] = heffF.x[c];
             y[c] = heffF.y[c];
@@ -138,7 +145,7 @@ struct Handle final : Base {
         }
     }
     void hdemag(double* x, double* y, double* z) override {
-        provider.compute(state.M, heffF, backend, nullptr);
+        provider.compute(state.M, heffF, *sb, nullptr);
         const auto& h = provider.lastDemagField();
         for (std::size_t c = 0; c < h.size(); ++c) {
             x[c] = h.x[c];
@@ -147,7 +154,7 @@ struct Handle final : Base {
         }
     }
     int relax(ref_sample* out, long cap, long* n) override {
-        auto res = dynamics::relax(state, provider, stepper, mat, backend, nullptr);
+        auto res = dynamics::relax(state, provider, stepper, mat, *sb, nullptr);
         state = res.state;
         long k = 0;
         for (const auto& s : res.log) {
@@ -179,13 +186,23 @@ struct Handle final : Base {
         state.step = s;
     }
     void energies(double out[5]) override {
-        provider.compute(state.M, heffF, backend, nullptr);
-        const EnergyBreakdown e = provider.energies(state.M, backend);
+        provider.compute(state.M, heffF, *sb, nullptr);
+        const EnergyBreakdown e = provider.energies(state.M, *sb);
         out[0] = e.exchange;
         out[1] = e.anisotropy;
         out[2] = e.demag;
         out[3] = e.zeeman;
         out[4] = e.total;
+    }
+    void setStepThreads(int threads) override {
+        if (threads <= 0) {
+            alt.reset();
+            sb = &backend;
+            return;
+        }
+        alt = std::make_unique<Backend>(threads == 1 ? BackendKind::serial : BackendKind::parallel,
+                                        static_cast<unsigned>(threads));
+        sb = alt.get();
     }
 };
 
@@ -262,6 +279,10 @@ int ref_sim_heff(void* h, double* x, double* y, double* z) {
 }
 int ref_sim_hdemag(void* h, double* x, double* y, double* z) {
     return guard([&] { static_cast<Base*>(h)->hdemag(x, y, z); });
+}
+// Step on a `threads`-thread backend from now on (<= 0: back to the creation backend).
+int ref_sim_set_step_threads(void* h, int threads) {
+    return guard([&] { static_cast<Base*>(h)->setStepThreads(threads); });
 }
 int ref_sim_energies(void* h, double out[5]) {
     return guard([&] { static_cast<Base*>(h)->energies(out); });

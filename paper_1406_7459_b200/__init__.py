@@ -102,6 +102,7 @@ def load_library() -> C.CDLL:
         "mfd_demag_field_f64": (C.c_int, [V, _PD, _PD, _PD]),
         "mfd_step": (C.c_int, [V, C.c_long, _PD, _PD]),
         "mfd_step_async": (C.c_int, [V, C.c_long]),
+        "mfd_prepare_async": (C.c_int, [V, C.c_long, C.POINTER(C.c_long)]),
         "mfd_sync": (C.c_int, [V]),
         "mfd_stream": (V, [V]),
         "mfd_relax": (C.c_int, [V, C.POINTER(C.c_int), _SampleCB, V]),
@@ -120,6 +121,7 @@ def load_library() -> C.CDLL:
         "mfd_device_state": (C.c_int, [V, C.POINTER(V), C.POINTER(C.c_longlong), C.POINTER(C.c_int)]),
         "mfd_launches_per_step": (C.c_int, [V]),
         "mfd_model_bytes_per_step": (C.c_double, [V]),
+        "mfd_debug_variants": (C.c_int, [V, C.c_char_p, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -315,6 +317,13 @@ class Simulation:
     def step_async(self, n: int):
         self._check(self.lib.mfd_step_async(self.h, n))
 
+    def prepare_async(self, n: int) -> int:
+        """Capture the graphs of the next step_async(n) without running them; returns
+        the kernel launches they contain."""
+        k = C.c_long()
+        self._check(self.lib.mfd_prepare_async(self.h, n, C.byref(k)))
+        return k.value
+
     def sync(self):
         self._check(self.lib.mfd_sync(self.h))
 
@@ -393,6 +402,13 @@ class Simulation:
 
     def model_bytes_per_step(self) -> float:
         return self.lib.mfd_model_bytes_per_step(self.h)
+
+    def variants(self) -> List[str]:
+        """Kernel template instantiations this context has enqueued (test hook)."""
+        n = self.lib.mfd_debug_variants(self.h, None, 0)
+        buf = C.create_string_buffer(n)
+        self.lib.mfd_debug_variants(self.h, buf, n)
+        return [l for l in buf.value.decode().split("\n") if l]
 
     @staticmethod
     def stability_dt_limit(grid: Grid, material: Material) -> float:

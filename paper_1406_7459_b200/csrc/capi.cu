@@ -3,7 +3,9 @@
 // the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 #include <new>
 #include <string>
@@ -153,6 +155,12 @@ mfd_status mfd_step(mfd_ctx* c, long n, double* last, double* all) {
     });
 }
 mfd_status mfd_step_async(mfd_ctx* c, long n) { return guard(c, [&] { ENG(c)->step_async(n); }); }
+mfd_status mfd_prepare_async(mfd_ctx* c, long n, long* launches) {
+    return guard(c, [&] {
+        const long k = ENG(c)->prepare_async(n);
+        if (launches) *launches = k;
+    });
+}
 mfd_status mfd_sync(mfd_ctx* c) { return guard(c, [&] { ENG(c)->sync(); }); }
 void* mfd_stream(mfd_ctx* c) { return (void*)c->eng->stream(); }
 mfd_status mfd_relax(mfd_ctx* c, int* converged, mfd_sample_cb cb, void* user) {
@@ -200,6 +208,15 @@ mfd_status mfd_device_state(mfd_ctx* c, void** m, long long* n, int* prec) {
     });
 }
 int mfd_launches_per_step(const mfd_ctx* c) { return c->eng->launches_per_step(); }
+int mfd_debug_variants(const mfd_ctx* c, char* buf, int len) {
+    const std::string v = c->eng->variants();
+    if (buf && len > 0) {
+        const size_t n = std::min<size_t>(v.size(), (size_t)len - 1);
+        std::memcpy(buf, v.data(), n);
+        buf[n] = 0;
+    }
+    return (int)v.size() + 1;
+}
 double mfd_model_bytes_per_step(const mfd_ctx* c) { return c->eng->model_bytes(); }
 
 } // extern "C"

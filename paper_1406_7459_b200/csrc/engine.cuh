@@ -8,8 +8,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <cstdarg>
 #include <map>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -149,6 +151,9 @@ public:
     virtual void field(int which, double*, double*, double*) = 0;
     virtual void step(long n, double* last, double* all) = 0;
     virtual void step_async(long n) = 0;
+    // Capture (without launching) the graphs the next step_async(n) will use;
+    // returns the number of kernel launches those graphs contain.
+    virtual long prepare_async(long n) = 0;
     virtual void sync() = 0;
     virtual bool relax(mfd_sample_cb cb, void* user) = 0;
     virtual mfd_sample sample_now() = 0;
@@ -161,6 +166,9 @@ public:
     virtual cudaStream_t stream() const = 0;
     virtual int launches_per_step() const = 0;
     virtual double model_bytes() const = 0;
+    // Kernel template instantiations enqueued since creation, one per line
+    // (test hook: lets the parity tests assert which production variant ran).
+    virtual std::string variants() const = 0;
     double t = 0;
     long stepno = 0;
     long long ncell = 0;
@@ -189,6 +197,7 @@ public:
     void field(int which, double* x, double* y, double* z) override;
     void step(long n, double* last, double* all) override;
     void step_async(long n) override;
+    long prepare_async(long n) override;
     void sync() override;
     bool relax(mfd_sample_cb cb, void* user) override;
     mfd_sample sample_now() override;
@@ -201,8 +210,23 @@ public:
     cudaStream_t stream() const override { return stream_; }
     int launches_per_step() const override { return terms_.demag ? 5 : 1; }
     double model_bytes() const override;
+    std::string variants() const override {
+        std::string o;
+        for (const auto& v : launched_) o += v + "\n";
+        return o;
+    }
 
 private:
+    void note(const char* fmt, ...) {
+        char b[256];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(b, sizeof b, fmt, ap);
+        va_end(ap);
+        launched_.insert(b);
+    }
+    static constexpr const char* tn() { return sizeof(T) == 4 ? "f32" : "f64"; }
+    std::set<std::string> launched_;
     void build_tensor_from_octant();
     void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr, bool skip_k1 = false,
                  bool fwd = false);
@@ -216,6 +240,8 @@ private:
     StepIO make_io(const Iter& it) const;
     Halo<T> halo_ptrs() const;
     void run_chunk(const std::vector<Iter>& its, int cur);
+    cudaGraphExec_t chunk_graph(const std::vector<Iter>& its, int cur);
+    std::vector<Iter> async_chunk(int K, long step0) const;
     void fetch_chunk(int n, std::vector<double>& torque, int& err);
     double torque_of(unsigned long long bits) const;
     mfd_sample make_sample(const double sums[8], double torque) const;
@@ -256,6 +282,12 @@ private:
     unsigned long long* h_torque_ = nullptr;   // pinned
     double* h_sums_ = nullptr;                 // pinned
     int* h_err_ = nullptr;                     // pinned
+    // step_async chunks not yet checked by sync(): the error word of chunk c
+    // lands in h_perr_[c] behind the chunk's graph
+    struct Pending { int K; long stepno; double t; int cur; };
+    static constexpr int kMaxPending = 1024;
+    std::vector<Pending> pending_;
+    int* h_perr_ = nullptr;                    // pinned [kMaxPending]
     T* h_stage_ = nullptr;                     // pinned 3N staging
     long long k5_blocks_ = 1;
     bool k1_pipe_ = false;                     // pipelined persistent K1 usable for this grid
@@ -284,6 +316,7 @@ private:
     static constexpr int kMaxChunk = 256;
 
     std::map<std::pair<std::vector<Iter>, int>, cudaGraphExec_t> graphs_;
+    std::map<std::pair<std::vector<Iter>, int>, int> graph_kernels_;   // kernel nodes per cached graph
 };
 
 } // namespace mfd

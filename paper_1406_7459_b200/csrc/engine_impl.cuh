@@ -162,6 +162,7 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     alloc(&torque_, kMaxChunk * sizeof(unsigned long long));
     alloc(&sums_, kMaxChunk * 8 * sizeof(double));
     alloc(&ticket_, sizeof(unsigned int));
+    ck(cudaMallocHost((void**)&h_perr_, kMaxPending * sizeof(int)), "host alloc");
     ck(cudaMemset(err_, 0, sizeof(int)), "memset");
     ck(cudaMemset(ticket_, 0, sizeof(unsigned int)), "memset");
     ck(cudaMemset(M_[0], 0, 3 * n * sizeof(T)), "memset");
@@ -343,6 +344,7 @@ Engine<T>::~Engine() {
     if (h_torque_) cudaFreeHost(h_torque_);
     if (h_sums_) cudaFreeHost(h_sums_);
     if (h_err_) cudaFreeHost(h_err_);
+    if (h_perr_) cudaFreeHost(h_perr_);
     if (h_stage_) cudaFreeHost(h_stage_);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -466,6 +468,7 @@ Halo<T> Engine<T>::halo_ptrs() const {
 
 template <class T>
 void Engine<T>::enq_local(const Iter& it, int cur) {
+    note("K5 k_local_llg<%s>", tn());
     k_local_llg<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
         geo_, M_[cur], M_[cur ^ 1], H_, lp_, make_io(it), make_ctl(it), halo_ptrs());
 }
@@ -478,22 +481,26 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
     if (!skip_k1) with_pow2(geo_.N, [&]<int L>() {
         using CF = XCfg<T, L>;
         if (k1_pipe_) {
-            if constexpr (L >= 2)
+            if constexpr (L >= 2) {
+                note("K1 k_r2c_x_pipe<%s,%d>", tn(), L);
                 k_r2c_x_pipe<T, L><<<k1_grid_, CF::NT, k1_smem_, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
+            }
         } else if (small_x_) {
             if constexpr (L >= 2 && L <= kSmallXMax) {
                 using CS = XCfg<T, L, 2>;
                 dim3 grid((unsigned)((nrows + 1) / 2), 3);
                 auto* k = geo_.G > 1 ? k_r2c_x<T, L, 2, true> : k_r2c_x<T, L, 2, false>;
+                note("K1 k_r2c_x<%s,%d,RS=2,MULTI=%d>", tn(), L, (int)(geo_.G > 1));
                 k<<<grid, CS::NT, CS::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
             }
         } else {
             dim3 grid((unsigned)((nrows + CF::ROWS - 1) / CF::ROWS), 3);
             auto* k = geo_.G > 1 ? k_r2c_x<T, L, 0, true> : k_r2c_x<T, L, 0, false>;
+            note("K1 k_r2c_x<%s,%d,RS=0,MULTI=%d>", tn(), L, (int)(geo_.G > 1));
             k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
         }
     });
-    if (ev) ck(cudaEventRecord(ev[1], stream_), "event");
+    if (ev) ck(cudaEventRecordWithFlags(ev[1], stream_, cudaEventRecordExternal), "event");
 }
 
 // B: K2 (y forward) -> K3 (z, tensor product, inverse z) -> K4 (y inverse) on
@@ -505,10 +512,11 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
         if (stop_after_ >= 2 && stop_after_ <= 3) return;
         with_yz([&]<int LY, int LZ>() {
             using CF = YZCfg<T, LY, LZ>;
+            note("K234 k_fft_yz_small<%s,%d,%d>", tn(), LY, LZ);
             k_fft_yz_small<T, LY, LZ><<<(geo_.Hx + CF::W - 1) / CF::W, CF::NT, CF::SMEM, stream_>>>(
                 geo_, A_, Kt_, tw_, ybuf_, ctl);
         });
-        if (ev) for (int q = 2; q <= 4; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
+        if (ev) for (int q = 2; q <= 4; ++q) ck(cudaEventRecordWithFlags(ev[q], stream_, cudaEventRecordExternal), "event");
         return;
     }
     const bool work = geo_.Hv > 0;
@@ -518,6 +526,7 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
                 using CF = YTCfg<T, L>;
                 const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
                 auto* k = 2 * geo_.ny == L ? k_fft_y_fwd_tma<T, L, true> : k_fft_y_fwd_tma<T, L, false>;
+                note("K2 k_fft_y_fwd_tma<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
                 k<<<k2_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmA_, B_, tw_, ctl, ntx, k2_box_);
             }
         });
@@ -525,55 +534,62 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
         with_pow2(Py_, [&]<int L>() {
             using CF = YCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+            note("K2 k_fft_y_fwd<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
             if (2 * geo_.ny == L)
                 k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
             else
                 k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
         });
     }
-    if (ev) ck(cudaEventRecord(ev[2], stream_), "event");
+    if (ev) ck(cudaEventRecordWithFlags(ev[2], stream_, cudaEventRecordExternal), "event");
     if (stop_after_ == 2) return;
     if (work) with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
             dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
+            note("K3 k_fft_z_conv1<%s,%d>", tn(), L);
             k_fft_z_conv1<T, L><<<grid, 64, 0, stream_>>>(geo_, B_, Kt_, ybuf_, ctl);
         } else if constexpr (z_variant<T, L>() == 2) {
             if (k3_srow_) {
                 using CF = Z2Cfg<T, L, true>;
                 dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Py_, 1);
                 auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true, true> : k_fft_z_conv2<T, L, false, true>;
+                note("K3 k_fft_z_conv2<%s,%d,FZ=%d,SROW=1>", tn(), L, (int)(2 * geo_.nzg == L));
                 k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
             } else {
                 using CF = Z2Cfg<T, L>;
                 dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
                 auto* k = 2 * geo_.nzg == L ? k_fft_z_conv2<T, L, true> : k_fft_z_conv2<T, L, false>;
+                note("K3 k_fft_z_conv2<%s,%d,FZ=%d,SROW=0>", tn(), L, (int)(2 * geo_.nzg == L));
                 k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
             }
         } else {
             using CF = ZCfg<T, L>;
             dim3 grid((geo_.Hv + CF::W - 1) / CF::W, Hy_, 1);
+            note("K3 k_fft_z_conv<%s,%d>", tn(), L);
             k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
         }
     });
-    if (ev) ck(cudaEventRecord(ev[3], stream_), "event");
+    if (ev) ck(cudaEventRecordWithFlags(ev[3], stream_, cudaEventRecordExternal), "event");
     if (stop_after_ == 3) return;
     if (work && k4_tma_) with_pow2(Py_, [&]<int L>() {
         if constexpr (YICfg<T, L>::OK) {
             using CF = YICfg<T, L>;
             const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
             auto* k = 2 * geo_.ny == L ? k_fft_y_inv_tma<T, L, true> : k_fft_y_inv_tma<T, L, false>;
+            note("K4 k_fft_y_inv_tma<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
             k<<<k4_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, Ar_, tw_, ctl, ntx);
         }
     });
     else if (work) with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
         dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+        note("K4 k_fft_y_inv<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
         if (2 * geo_.ny == L)
             k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
         else
             k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
     });
-    if (ev) ck(cudaEventRecord(ev[4], stream_), "event");
+    if (ev) ck(cudaEventRecordWithFlags(ev[4], stream_, cudaEventRecordExternal), "event");
 }
 
 // C: K5 (x inverse + H_eff + LLG + Euler) on A_ (the receive side of the second transpose)
@@ -596,6 +612,8 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
                                          : k_c2r_x_llg_v<T, L, false, 1, false, true>)
                           : io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 1, true> : k_c2r_x_llg_v<T, L, true, 1, false>)
                                     : (fwd ? k_c2r_x_llg_v<T, L, false, 1, true> : k_c2r_x_llg_v<T, L, false, 1, false>);
+                note("K5 k_c2r_x_llg_v<%s,%d,SUMS=%d,RS=1,FWD=%d,MULTI=%d>", tn(), L, (int)(io.sums != 0),
+                     (int)(fwd && geo_.G == 1), (int)(geo_.G > 1));
                 k<<<(unsigned)nrows, CS::NT, CS::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
                 return;
             }
@@ -607,9 +625,12 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
                     : io.sums ? (fwd ? k_c2r_x_llg_v<T, L, true, 0, true> : k_c2r_x_llg_v<T, L, true, 0, false>)
                               : (fwd ? k_c2r_x_llg_v<T, L, false, 0, true> : k_c2r_x_llg_v<T, L, false, 0, false>);
             const int smem = fwd && !multi ? k5_smem<T, L, 0, true>() : k5_smem<T, L, 0, false>();
+            note("K5 k_c2r_x_llg_v<%s,%d,SUMS=%d,RS=0,FWD=%d,MULTI=%d>", tn(), L, (int)(io.sums != 0),
+                 (int)(fwd && !multi), (int)multi);
             k<<<grid, CF::NT, smem, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
         } else {
             auto* k = multi ? k_c2r_x_llg<T, L, true> : k_c2r_x_llg<T, L, false>;
+            note("K5 k_c2r_x_llg<%s,%d,MULTI=%d>", tn(), L, (int)multi);
             k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, A_, Mc, Mn, H_, tw_, scale_, lp_, io, ctl, hl);
         }
     });
@@ -621,14 +642,14 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
 template <class T>
 void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, bool skip_k1, bool fwd) {
     const size_t tsz = sizeof(T);
-    if (events) ck(cudaEventRecord(ev[0], stream_), "event");
+    if (events) ck(cudaEventRecordWithFlags(ev[0], stream_, cudaEventRecordExternal), "event");
     if (tr_ && slab_.world > 1)
         tr_->halo(M_[cur], geo_.ncell * tsz, (size_t)grid_.nx * grid_.ny * tsz, geo_.nz, halo_,
                   halo_ + 3LL * grid_.nx * grid_.ny, stream_);
     if (!terms_.demag) {
         enq_local(it, cur);
         if (events)
-            for (int q = 1; q < 6; ++q) ck(cudaEventRecord(ev[q], stream_), "event");
+            for (int q = 1; q < 6; ++q) ck(cudaEventRecordWithFlags(ev[q], stream_, cudaEventRecordExternal), "event");
     } else {
         enq_A(it, cur, events ? ev : nullptr, skip_k1);
         if (stop_after_ == 1) return;
@@ -639,7 +660,7 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, b
         // transpose #2 (inverse): back to this rank's planes, all x-bins
         if (tr_ && slab_.world > 1) tr_->alltoall(Ar_, A_, geo_.SA * sizeof(C2<T>), stream_);
         enq_C(it, cur, events ? ev : nullptr, fwd);
-        if (events) ck(cudaEventRecord(ev[5], stream_), "event");
+        if (events) ck(cudaEventRecordWithFlags(ev[5], stream_, cudaEventRecordExternal), "event");
     }
     if (tr_ && slab_.world > 1) {
         tr_->allreduce_max_u64(torque_ + it.slot, 1, stream_);
@@ -648,19 +669,23 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, b
     }
 }
 
-// Launch a chunk of iterations (one CUDA graph, cached by its shape).
+// The CUDA graph of a chunk of iterations (captured once, cached by its shape).
 template <class T>
-void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
+cudaGraphExec_t Engine<T>::chunk_graph(const std::vector<Iter>& its, int cur) {
     auto key = std::make_pair(its, cur);
     auto f = graphs_.find(key);
     if (f == graphs_.end()) {
         if (graphs_.size() > 64) {
             for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
             graphs_.clear();
+            graph_kernels_.clear();
         }
         cudaGraph_t g;
         ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
         cudaMemsetAsync(torque_, 0, its.size() * sizeof(unsigned long long), stream_);
+        // a launch that halted part-way (error flag raised by an earlier CTA)
+        // leaves the last-block ticket short; every graph starts from zero
+        cudaMemsetAsync(ticket_, 0, sizeof(unsigned int), stream_);
         int c = cur;
         bool fused_prev = false;
         for (size_t j = 0; j < its.size(); ++j) {
@@ -673,12 +698,29 @@ void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
             if (it.update) c ^= 1;
         }
         ck(cudaStreamEndCapture(stream_, &g), "end capture");
+        size_t nn = 0;
+        ck(cudaGraphGetNodes(g, nullptr, &nn), "graph nodes");
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) ck(cudaGraphGetNodes(g, nodes.data(), &nn), "graph nodes");
+        int nk = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            ck(cudaGraphNodeGetType(nd, &ty), "node type");
+            nk += ty == cudaGraphNodeTypeKernel;
+        }
+        graph_kernels_[key] = nk;
         cudaGraphExec_t ex;
         ck(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
         cudaGraphDestroy(g);
         f = graphs_.emplace(key, ex).first;
     }
-    ck(cudaGraphLaunch(f->second, stream_), "graph launch");
+    return f->second;
+}
+
+// Launch a chunk of iterations.
+template <class T>
+void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
+    ck(cudaGraphLaunch(chunk_graph(its, cur), stream_), "graph launch");
 }
 
 template <class T>
@@ -875,19 +917,48 @@ void Engine<T>::step(long n, double* last, double* all) {
     }
 }
 
+// Iterations of a K-step step_async chunk starting at step count step0:
+// renormalise iff (step+1) % renormalizeEvery == 0 (sim.hpp:38).
+template <class T>
+std::vector<Iter> Engine<T>::async_chunk(int K, long step0) const {
+    std::vector<Iter> its(K);
+    for (int i = 0; i < K; ++i) {
+        its[i].slot = i;
+        its[i].renorm = ((step0 + i + 1) % st_.renorm_every) == 0;
+    }
+    return its;
+}
+
+template <class T>
+long Engine<T>::prepare_async(long n) {
+    long done = 0, s0 = stepno, launches = 0;
+    int c = cur_;
+    while (done < n) {
+        const int K = (int)std::min<long>(n - done, 64);
+        const std::vector<Iter> its = async_chunk(K, s0);
+        chunk_graph(its, c);
+        launches += graph_kernels_[std::make_pair(its, c)];
+        s0 += K;
+        c ^= K & 1;
+        done += K;
+    }
+    return launches;
+}
+
 template <class T>
 void Engine<T>::step_async(long n) {
     // Benchmark path: whole graphs of 64 steps, no host round trip; the
-    // renormalisation pattern is fixed per graph.
+    // renormalisation pattern is fixed per graph.  The host clock advances
+    // optimistically; each chunk's error word is copied out behind it, so
+    // sync() can roll t / stepno / cur_ back to the last completed step.
     long done = 0;
     while (done < n) {
         const int K = (int)std::min<long>(n - done, 64);
-        std::vector<Iter> its(K);
-        for (int i = 0; i < K; ++i) {
-            its[i].slot = i;
-            its[i].renorm = ((stepno + i + 1) % st_.renorm_every) == 0;
-        }
+        const std::vector<Iter> its = async_chunk(K, stepno);
+        if ((int)pending_.size() == kMaxPending) sync();
         run_chunk(its, cur_);
+        ck(cudaMemcpyAsync(h_perr_ + pending_.size(), err_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+        pending_.push_back(Pending{K, stepno, t, cur_});
         for (int i = 0; i < K; ++i) {
             t += st_.dt;
             stepno += 1;
@@ -901,8 +972,22 @@ template <class T>
 void Engine<T>::sync() {
     ck(cudaMemcpyAsync(h_err_, err_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
     ck(cudaStreamSynchronize(stream_), "sync");
+    std::vector<Pending> pend;
+    pend.swap(pending_);
     if (*h_err_) {
         cudaMemsetAsync(err_, 0, sizeof(int), stream_);
+        // the first chunk whose error word is set failed at iteration err - 1;
+        // later chunks halted on the device (the word is never cleared in between)
+        for (size_t c = 0; c < pend.size(); ++c) {
+            if (!h_perr_[c]) continue;
+            const Pending& p = pend[c];
+            const int ok = std::min(h_perr_[c] - 1, p.K);
+            t = p.t;
+            for (int i = 0; i < ok; ++i) t += st_.dt;   // same accumulation as step()
+            stepno = p.stepno + ok;
+            cur_ = p.cur ^ (ok & 1);
+            break;
+        }
         throw Error(MFD_ENONFINITE, "eulerUpdate: non-finite magnetization after step (time step too large?)");
     }
 }
@@ -1020,13 +1105,25 @@ void Engine<T>::debug_stage(int stage, double* out) {
 template <class T>
 void Engine<T>::timing(double ms[7]) {
     // One real Simulation::step with an event after every pass (advances the state).
+    // The pass boundaries are event-record nodes of a captured one-iteration
+    // graph, so the passes run exactly as inside the step graphs.
     cudaEvent_t ev[6];
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
     Iter it;
     it.update = 1;
     it.renorm = ((stepno + 1) % st_.renorm_every) == 0;
-    ck(cudaMemsetAsync(torque_, 0, sizeof(unsigned long long), stream_), "memset");
+    cudaGraph_t g;
+    ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+    cudaMemsetAsync(torque_, 0, sizeof(unsigned long long), stream_);
+    cudaMemsetAsync(ticket_, 0, sizeof(unsigned int), stream_);
     enqueue(it, cur_, true, ev);
+    ck(cudaStreamEndCapture(stream_, &g), "end capture");
+    cudaGraphExec_t ex;
+    ck(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    const cudaError_t le = cudaGraphLaunch(ex, stream_);
+    cudaGraphExecDestroy(ex);
+    ck(le, "graph launch");
     std::vector<double> tq;
     int err = 0;
     fetch_chunk(1, tq, err);
@@ -1036,11 +1133,11 @@ void Engine<T>::timing(double ms[7]) {
     cur_ ^= 1;
     for (int q = 0; q < 5; ++q) {
         float f = 0;
-        cudaEventElapsedTime(&f, ev[q], ev[q + 1]);
+        ck(cudaEventElapsedTime(&f, ev[q], ev[q + 1]), "event time");
         ms[q] = f;
     }
     float tot = 0;
-    cudaEventElapsedTime(&tot, ev[0], ev[5]);
+    ck(cudaEventElapsedTime(&tot, ev[0], ev[5]), "event time");
     ms[5] = tot;
     ms[6] = 0;
     for (auto& e : ev) cudaEventDestroy(e);

@@ -50,6 +50,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_Z2_W
 #define MFD_Z2_W 0             // K3 (two-stage) columns per CTA override (0: default)
 #endif
+#ifndef MFD_K3_ASYNC
+#define MFD_K3_ASYNC 1         // K3 stage-0 inputs of all three components in flight at once (cp.async)
+#endif
 #ifndef MFD_K5_STG_MINB
 #define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
 #endif
@@ -303,6 +306,16 @@ __device__ __forceinline__ int yswz(int pos) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// one complex element, global -> shared, asynchronously
+template <class T>
+__device__ __forceinline__ void cp_async_c2(C2<T>* smem, const C2<T>* gmem) {
+    if constexpr (sizeof(C2<T>) == 16) cp_async16(smem, gmem);
+    else cp_async8(smem, gmem);
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int K>
@@ -787,11 +800,45 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     // smem column of (comp c, row r, bin w): c*CO + r*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + (SROW ? 0 : r * W) + w;
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
+    if constexpr (MFD_K3_ASYNC) {
+        // All three components' inputs go into flight at kernel entry as
+        // cp.async copies into the thread's own shared-memory slots (the
+        // positions R1*j + n2 its stage-0 task reads and then overwrites), one
+        // commit group per component: no staging registers, and the HBM
+        // latency of components 1 and 2 hides behind component 0's DFT.
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+#pragma unroll
+            for (int j = 0; j < R0 / 2; ++j) {
+                const int pos = R1 * j + n2;
+                C2<T>* d = scol + pos * NCOL + c * CO;
+                if (live && (FZ || pos < nz)) cp_async_c2<T>(d, gcol + c * cstride + (long long)pos * g.S_k);
+                else *d = mk<T>(0, 0);
+            }
+            cp_commit();
+        }
+        C2<T> twr[R0];
+#pragma unroll
+        for (int k = 1; k < R0; ++k) twr[k] = __ldg(tw_dense<T, L>(tw) + n2 * k);
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c) {
+            if (c == 0) cp_wait<2>();
+            else if (c == 1) cp_wait<1>();
+            else cp_wait<0>();
+            C2<T> x[R0];
+#pragma unroll
+            for (int j = 0; j < R0; ++j) x[j] = 2 * j < R0 ? scol[(R1 * j + n2) * NCOL + c * CO] : mk<T>(0, 0);
+            dft<T, R0, false, true>(x);
+#pragma unroll
+            for (int k = 1; k < R0; ++k) x[k] = cmul<T>(x[k], twr[k]);
+#pragma unroll
+            for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * CO] = x[k];
+        }
+    } else {
     // Software pipeline over the three components: the loads of component
     // c+1 are in flight while component c is transformed.  (A persistent
     // variant that also prefetched the next tile measured slower on B200:
     // 0.88 vs 0.69 ms at 512x512x64 f32, the tensor loads lost their overlap.)
-    {
     C2<T> nxt[R0 / 2];
     auto fetch = [&](int c) {
 #pragma unroll
@@ -1405,7 +1452,13 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // STG: ms = the staged copy of this row (component 0, x = 0) in shared
 // memory, component stride mcs, row pitch mpitch (rows j-1 and j+1 of the
 // same plane are the adjacent staged rows).
-template <class T, bool SUMS, bool STG = false>
+// FAST: fused multiply-adds, an approximate reciprocal square root for the
+// renormalisation and the torque max in T (the production K5; the bitwise
+// reference-order form stays in cell_update / k_local_llg and FAST = false).
+#ifndef MFD_K5_FAST
+#define MFD_K5_FAST 1
+#endif
+template <class T, bool SUMS, bool STG = false, bool FAST = MFD_K5_FAST>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                           const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
                                           const Halo<T>& hl, long long c0, int i0, int j, int k,
@@ -1449,12 +1502,16 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             const T mc = m[c][q];
             const T xm = q > 0 ? m[c][q - 1] : xl, xp = q < V - 1 ? m[c][q + 1] : xr;
             T h = 0;
-            if (q > 0 || hx0) h = add_rn(h, mul_rn(P.cx, sub_rn(xm, mc)));
-            if (q < V - 1 || hx1) h = add_rn(h, mul_rn(P.cx, sub_rn(xp, mc)));
-            if (hy0) h = add_rn(h, mul_rn(P.cy, sub_rn(ym[q], mc)));
-            if (hy1) h = add_rn(h, mul_rn(P.cy, sub_rn(yp[q], mc)));
-            if (hz0) h = add_rn(h, mul_rn(P.cz, sub_rn(zm[q], mc)));
-            if (hz1) h = add_rn(h, mul_rn(P.cz, sub_rn(zp[q], mc)));
+            auto ex = [&](T w, T nb) {   // fields.hpp:33-48: h += w (M_nbr - M_c)
+                if constexpr (FAST) h = fma_rn(w, sub_rn(nb, mc), h);
+                else h = add_rn(h, mul_rn(w, sub_rn(nb, mc)));
+            };
+            if (q > 0 || hx0) ex(P.cx, xm);
+            if (q < V - 1 || hx1) ex(P.cx, xp);
+            if (hy0) ex(P.cy, ym[q]);
+            if (hy1) ex(P.cy, yp[q]);
+            if (hz0) ex(P.cz, zm[q]);
+            if (hz1) ex(P.cz, zp[q]);
             H[c][q] = add_rn(hd[c][q], h);
             if (SUMS) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
                 if (q < V - 1 || hx1) { const double e = (double)xp - mc; elink[q] += P.wx * e * e; }
@@ -1465,10 +1522,65 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
     }
     T mo[3][V];
     bool all = true;
+    T tmv = 0;   // FAST: max |rhs|^2 of the V cells in T
 #pragma unroll
     for (int q = 0; q < V; ++q) {
         const T mx = m[0][q], my = m[1][q], mz = m[2][q];
         T Hx = H[0][q], Hy = H[1][q], Hz = H[2][q];
+        if constexpr (FAST) {
+            if (P.anis) {
+                const T proj = mul_rn(P.ca, fma_rn(mx, P.ax, fma_rn(my, P.ay, mul_rn(mz, P.az))));
+                Hx = fma_rn(proj, P.ax, Hx);
+                Hy = fma_rn(proj, P.ay, Hy);
+                Hz = fma_rn(proj, P.az, Hz);
+            }
+            if (P.zee) {
+                Hx = add_rn(Hx, P.hx);
+                Hy = add_rn(Hy, P.hy);
+                Hz = add_rn(Hz, P.hz);
+            }
+            if (io.write_h == 1) { H[0][q] = Hx; H[1][q] = Hy; H[2][q] = Hz; }
+            if (SUMS) {
+                acc[0] += (double)mx;
+                acc[1] += (double)my;
+                acc[2] += (double)mz;
+                acc[3] += elink[q];
+                const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
+                const double pp = m0 * P.dax + m1 * P.day + m2 * P.daz;
+                acc[4] += 1.0 - pp * pp;
+                acc[5] += (double)hd[0][q] * mx + (double)hd[1][q] * my + (double)hd[2][q] * mz;
+                acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
+            }
+            // llgRhs (dynamics.hpp:49-64): b = mu0 H, c = m x b, d = m x c, r = P c + D d
+            const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
+            const T c0x = fma_rn(my, b2, -mul_rn(mz, b1));
+            const T c1x = fma_rn(mz, b0, -mul_rn(mx, b2));
+            const T c2x = fma_rn(mx, b1, -mul_rn(my, b0));
+            const T d0 = fma_rn(my, c2x, -mul_rn(mz, c1x));
+            const T d1 = fma_rn(mz, c0x, -mul_rn(mx, c2x));
+            const T d2 = fma_rn(mx, c1x, -mul_rn(my, c0x));
+            const T r0 = fma_rn(P.precess, c0x, mul_rn(P.damp, d0));
+            const T r1 = fma_rn(P.precess, c1x, mul_rn(P.damp, d1));
+            const T r2 = fma_rn(P.precess, c2x, mul_rn(P.damp, d2));
+            tmv = fmax(tmv, fma_rn(r0, r0, fma_rn(r1, r1, mul_rn(r2, r2))));
+            // eulerUpdate (dynamics.hpp:93-121)
+            T e0 = fma_rn(P.dt, r0, mx);
+            T e1 = fma_rn(P.dt, r1, my);
+            T e2 = fma_rn(P.dt, r2, mz);
+            if (io.renorm) {
+                const T n2 = fma_rn(e0, e0, fma_rn(e1, e1, mul_rn(e2, e2)));
+                if (!(n2 > T(0)) || !isfinite(n2)) {
+                    all = false;
+                } else {
+                    const T f = mul_rn(P.Ms, rsqrt_(n2));
+                    e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
+                }
+            } else if (!isfinite(add_rn(add_rn(e0, e1), e2))) {
+                all = false;
+            }
+            mo[0][q] = e0; mo[1][q] = e1; mo[2][q] = e2;
+            continue;
+        }
         if (P.anis) {
             const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
             Hx = add_rn(Hx, mul_rn(proj, P.ax));
@@ -1522,6 +1634,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         }
         mo[0][q] = e0; mo[1][q] = e1; mo[2][q] = e2;
     }
+    if constexpr (FAST) tmax = fmax(tmax, (double)tmv);
     if (io.write_h) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) vstore<T>(Hout + c * n + c0, io.write_h == 1 ? H[c] : hd[c]);

@@ -103,6 +103,9 @@ public:
         }
     }
     void step_async(long n) override { step(n, nullptr, nullptr); }
+    long prepare_async(long n) override {
+        return n * world_ * (long)ranks_[0]->launches_per_step();   // eager: no graphs
+    }
     void sync() override { ck(cudaStreamSynchronize(stream_), "sync"); }
 
     bool relax(mfd_sample_cb cb, void* user) override {
@@ -156,6 +159,20 @@ public:
     cudaStream_t stream() const override { return stream_; }
     int launches_per_step() const override { return world_ * ranks_[0]->launches_per_step(); }
     double model_bytes() const override { return world_ * ranks_[0]->model_bytes(); }
+    std::string variants() const override {
+        std::set<std::string> all;
+        for (const auto& e : ranks_) {
+            const std::string v = e->variants();
+            size_t a = 0, b;
+            while ((b = v.find('\n', a)) != std::string::npos) {
+                all.insert(v.substr(a, b - a));
+                a = b + 1;
+            }
+        }
+        std::string o;
+        for (const auto& v : all) o += v + "\n";
+        return o;
+    }
 
 private:
     void advance() {
@@ -177,6 +194,7 @@ private:
         for (auto& e : ranks_) {
             ck(cudaMemsetAsync(e->torque_, 0, sizeof(unsigned long long), stream_), "memset");
             ck(cudaMemsetAsync(e->err_, 0, sizeof(int), stream_), "memset");
+            ck(cudaMemsetAsync(e->ticket_, 0, sizeof(unsigned int), stream_), "memset");
         }
         // halo: lo of r <- top plane of r-1, hi of r <- bottom plane of r+1 (per component)
         for (int r = 0; r < world_; ++r) {

@@ -269,3 +269,26 @@ def test_set_get_roundtrip_and_uniform():
     u = E.Simulation(g, E.Material(Ms=MS), init_direction=(0.6, 0.0, 0.8))
     mm = u.get_m()
     assert np.all(mm[0] == MS * 0.6) and np.all(mm[2] == MS * 0.8)
+
+
+def test_step_async_error_rolls_back_clock():
+    """A non-finite update inside an asynchronous chunk: sync() raises the reference's
+    runtime_error and t / step stop at the last completed step (dynamics.hpp:115-120),
+    across several 64-step graph chunks."""
+    s = spec_of((4, 4, 4, 2e-9, 2e-9, 2e-9), dt=2e-12, renorm_every=100000)
+    # |M| grows under Euler without renormalisation; from 3% of Ms it overflows at
+    # step 97 of the reference, i.e. inside the second 64-step graph chunk
+    m0 = 0.03 * np.full((3, s.n), MS / 3 ** 0.5)
+    sim, ref, m = pair(s, 64, m=m0)
+    n_ok = 0
+    with pytest.raises(RuntimeError):
+        for _ in range(400):
+            ref.step(1)
+            n_ok += 1
+    sim.step_async(400)
+    with pytest.raises(RuntimeError, match="eulerUpdate: non-finite magnetization"):
+        sim.sync()
+    assert sim.time() == ref.time()
+    assert sim.time()[1] == n_ok
+    assert np.all(np.isfinite(sim.get_m()))
+    sim.sync()   # error consumed
