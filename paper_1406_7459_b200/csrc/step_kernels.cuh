@@ -1452,11 +1452,14 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // STG: ms = the staged copy of this row (component 0, x = 0) in shared
 // memory, component stride mcs, row pitch mpitch (rows j-1 and j+1 of the
 // same plane are the adjacent staged rows).
-// FAST: fused multiply-adds, an approximate reciprocal square root for the
-// renormalisation and the torque max in T (the production K5; the bitwise
+// FAST: fused multiply-adds and an approximate reciprocal square root for the
+// renormalisation (the production K5; the bitwise
 // reference-order form stays in cell_update / k_local_llg and FAST = false).
 #ifndef MFD_K5_FAST
-#define MFD_K5_FAST 1
+#define MFD_K5_FAST 0   // measured at C4 f32: FMA epilogue 0.384 vs 0.377 ms (strict), kept for A/B
+#endif
+#ifndef MFD_K5_ASYNC
+#define MFD_K5_ASYNC 0   // cp.async-staged spectrum rows: 0.395 vs 0.384 ms at C4 f32 (register loads win)
 #endif
 template <class T, bool SUMS, bool STG = false, bool FAST = MFD_K5_FAST>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
@@ -1522,7 +1525,6 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
     }
     T mo[3][V];
     bool all = true;
-    T tmv = 0;   // FAST: max |rhs|^2 of the V cells in T
 #pragma unroll
     for (int q = 0; q < V; ++q) {
         const T mx = m[0][q], my = m[1][q], mz = m[2][q];
@@ -1562,7 +1564,10 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             const T r0 = fma_rn(P.precess, c0x, mul_rn(P.damp, d0));
             const T r1 = fma_rn(P.precess, c1x, mul_rn(P.damp, d1));
             const T r2 = fma_rn(P.precess, c2x, mul_rn(P.damp, d2));
-            tmv = fmax(tmv, fma_rn(r0, r0, fma_rn(r1, r1, mul_rn(r2, r2))));
+            {   // maxTorqueRate in double (dynamics.hpp:75-82): |rhs|^2 overflows float
+                const double v0 = r0, v1 = r1, v2 = r2;
+                tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
+            }
             // eulerUpdate (dynamics.hpp:93-121)
             T e0 = fma_rn(P.dt, r0, mx);
             T e1 = fma_rn(P.dt, r1, my);
@@ -1634,7 +1639,6 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         }
         mo[0][q] = e0; mo[1][q] = e1; mo[2][q] = e2;
     }
-    if constexpr (FAST) tmax = fmax(tmax, (double)tmv);
     if (io.write_h) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) vstore<T>(Hout + c * n + c0, io.write_h == 1 ? H[c] : hd[c]);
@@ -1713,20 +1717,6 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
     constexpr int HP = N / 2 > 0 ? N / 2 : 1;
     constexpr int ITEMS = NCOL * HP;
     constexpr int IT = (ITEMS + NT - 1) / NT;
-    C2<T> pa[IT], pb[IT], pc[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        const int e = threadIdx.x + it * NT;
-        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
-        const long long row = row0 + col % ROWS;
-        pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
-        if (e < ITEMS && row < nrows) {
-            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
-            pa[it] = *abin<MULTI>(g, src, k);
-            pb[it] = *abin<MULTI>(g, src, N - k);
-            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, src, N / 2);
-        }
-    }
     auto pre = [&](C2<T>* scol, int k, C2<T> a, C2<T> b) {
         const C2<T> w = __ldg(tw_dense<T, 2 * N>(tw) + k);
         {
@@ -1741,6 +1731,51 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
             scol[xpad<T>(N - k)] = mk<T>(s.x - wd.y, s.y + wd.x);
         }
     };
+    if constexpr (MFD_K5_ASYNC && N >= 2) {
+        // The CTA's NCOL spectrum rows (N+1 bins each) land in shared memory by
+        // cp.async at their padded positions (no staging registers: all of the
+        // CTA's HBM reads are in flight at once), then each thread turns its
+        // pairs (k, N-k) into the C2R input in place: a pair is read and written
+        // by one thread only, and bin N/2 / bin N belong to the k = 0 owner.
+        constexpr int RL = N + 1;
+        for (int e = threadIdx.x; e < NCOL * RL; e += NT) {
+            const int col = e / RL, k = e - (e / RL) * RL;
+            const long long row = row0 + col % ROWS;
+            C2<T>* d = sm + col * LP + xpad<T>(k);
+            if (row < nrows) cp_async_c2<T>(d, abin<MULTI>(g, A + ((long long)(col / ROWS) * nrows + row) * g.Hp, k));
+            else *d = mk<T>(0, 0);
+        }
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+#pragma unroll 4
+        for (int e = threadIdx.x; e < ITEMS; e += NT) {
+            const int col = e / HP, k = e - (e / HP) * HP;
+            C2<T>* scol = sm + col * LP;
+            const C2<T> a = scol[xpad<T>(k)], b = scol[xpad<T>(N - k)];
+            if (k == 0) {
+                const C2<T> c = scol[xpad<T>(N / 2)];
+                pre(scol, 0, a, b);
+                pre(scol, N / 2, c, c);
+            } else {
+                pre(scol, k, a, b);
+            }
+        }
+    } else {
+    C2<T> pa[IT], pb[IT], pc[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const int e = threadIdx.x + it * NT;
+        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+        const long long row = row0 + col % ROWS;
+        pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
+        if (e < ITEMS && row < nrows) {
+            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
+            pa[it] = *abin<MULTI>(g, src, k);
+            pb[it] = *abin<MULTI>(g, src, N - k);
+            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, src, N / 2);
+        }
+    }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
         const int e = threadIdx.x + it * NT;
@@ -1748,6 +1783,7 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
         const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
         pre(sm + col * LP, k, pa[it], pb[it]);
         if (k == 0 && N > 1) pre(sm + col * LP, N / 2, pc[it], pc[it]);
+    }
     }
     __syncthreads();
     if constexpr (Plan<T, N>::S > 0) {
