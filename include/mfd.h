@@ -87,7 +87,12 @@ typedef struct {
     int world;
     int rank;
     int virtual_ranks;
-    int reserved[3];
+    /* world > 1, virtual_ranks = 0: 0 = NCCL over NVLink (production); 1 = host-staged
+     * shared-memory transport (test harness: the one-process-per-GPU path with several
+     * processes on ONE GPU, which NCCL refuses; the first 16 bytes of nccl_id name the
+     * segment, any random bytes shared by the ranks). */
+    int transport;
+    int reserved[2];
     unsigned char nccl_id[128];
 } mfd_exec;
 

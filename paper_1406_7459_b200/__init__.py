@@ -61,7 +61,8 @@ class _Stepper(C.Structure):
 
 class _Exec(C.Structure):
     _fields_ = [("precision_bits", C.c_int), ("device", C.c_int), ("world", C.c_int), ("rank", C.c_int),
-                ("virtual_ranks", C.c_int), ("reserved", C.c_int * 3), ("nccl_id", C.c_ubyte * 128)]
+                ("virtual_ranks", C.c_int), ("transport", C.c_int), ("reserved", C.c_int * 2),
+                ("nccl_id", C.c_ubyte * 128)]
 
 
 class _Sample(C.Structure):
@@ -217,10 +218,12 @@ class Simulation:
     def __init__(self, grid: Grid, material: Material, fields: FieldConfig = FieldConfig(),
                  stepper: StepperConfig = StepperConfig(), precision: int = 64, device: int = 0,
                  init_direction: Sequence[float] = (0.0, 0.0, 1.0), world: int = 1, rank: int = 0,
-                 virtual_ranks: bool = False, nccl_id: Optional[bytes] = None):
+                 virtual_ranks: bool = False, nccl_id: Optional[bytes] = None, transport: str = "nccl"):
         """world > 1: z-slab decomposition (mfd.h mfd_exec).  virtual_ranks runs
-        all slabs on `device`; otherwise one process per GPU over NCCL, with
-        set_m / get_m moving this rank's slab."""
+        all slabs on `device`; otherwise one process per rank, with set_m / get_m
+        moving this rank's slab, over NCCL (transport="nccl", one GPU each) or the
+        host-staged shared-memory test transport (transport="shm", any number of
+        processes on one GPU; nccl_id = shared random bytes naming the segment)."""
         self.lib = load_library()
         self.grid, self.material, self.fields, self.stepper = grid, material, fields, stepper
         self.precision = precision
@@ -233,7 +236,9 @@ class Simulation:
                          int(fields.zeeman), (C.c_double * 3)(*fields.extern_field))
         self._s = _Stepper(stepper.dt, stepper.renormalize_every, stepper.max_steps,
                            stepper.torque_tol_deg_per_ns, stepper.sample_every)
-        self._e = _Exec(precision, device, world, rank, int(virtual_ranks))
+        if transport not in ("nccl", "shm"):
+            raise ValueError("transport must be 'nccl' or 'shm'")
+        self._e = _Exec(precision, device, world, rank, int(virtual_ranks), 1 if transport == "shm" else 0)
         if nccl_id is not None:
             C.memmove(self._e.nccl_id, bytes(nccl_id), 128)
         h = C.c_void_p()

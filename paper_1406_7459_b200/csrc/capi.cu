@@ -94,9 +94,16 @@ mfd_status mfd_create(const mfd_grid* grid, const mfd_material* mat, const mfd_t
             c->eng.reset(prec == 32 ? mfd::make_virtual_group<float>(*grid, *mat, *terms, *stepper, dev, world)
                                     : mfd::make_virtual_group<double>(*grid, *mat, *terms, *stepper, dev, world));
         } else {
-            mfd::Transport* tr = world > 1 ? mfd::make_nccl_transport(exec->nccl_id, rank, world, dev) : nullptr;
-            c->eng.reset(prec == 32 ? mfd::make_engine<float>(*grid, *mat, *terms, *stepper, dev, rank, world, tr)
-                                    : mfd::make_engine<double>(*grid, *mat, *terms, *stepper, dev, rank, world, tr));
+            if (world > 1 && exec->transport != 0 && exec->transport != 1)
+                throw mfd::Error(MFD_EINVAL, "mfd_create: transport must be 0 (NCCL) or 1 (shared memory)");
+            std::unique_ptr<mfd::Transport> tr;
+            if (world > 1)
+                tr.reset(exec->transport == 1 ? mfd::make_shm_transport(exec->nccl_id, rank, world)
+                                              : mfd::make_nccl_transport(exec->nccl_id, rank, world, dev));
+            // ownership of the transport passes to the engine (released by it on failure too)
+            mfd::Transport* t = tr.release();
+            c->eng.reset(prec == 32 ? mfd::make_engine<float>(*grid, *mat, *terms, *stepper, dev, rank, world, t)
+                                    : mfd::make_engine<double>(*grid, *mat, *terms, *stepper, dev, rank, world, t));
         }
         *out = c.release();
     });

@@ -86,9 +86,12 @@ template <class T> __global__ void k_ybuf(int Py, int Hy, int* out);
 // passes, on its own stream (so they are captured into the step graphs).
 struct Transport {
     virtual ~Transport() = default;
-    // all-to-all of `world` equal contiguous blocks: block p of send -> rank p,
-    // block q of recv <- rank q.
-    virtual void alltoall(const void* send, void* recv, size_t blk_bytes, cudaStream_t s) = 0;
+    // Called once by the engine with the largest all-to-all block and halo
+    // plane it will move (before any transfer is enqueued).
+    virtual void reserve(size_t /*blk_bytes*/, size_t /*plane_bytes*/) {}
+    // all-to-all of `world` equal contiguous blocks of blk_bytes, block p at
+    // send + p * stride -> rank p, block q of recv (recv + q * stride) <- rank q.
+    virtual void alltoall(const void* send, void* recv, size_t blk_bytes, size_t stride, cudaStream_t s) = 0;
     // one-plane halo of the slab: planes 0 / nzl-1 of each component (stride
     // comp_stride bytes, plane_bytes each) go to rank-1 / rank+1; the
     // neighbours' planes land in lo / hi ([3][plane]).
@@ -101,6 +104,11 @@ struct Transport {
 };
 // NCCL transport over NVLink/NVSwitch (nccl_transport.cu).
 Transport* make_nccl_transport(const unsigned char id[128], int rank, int world, int device);
+// Host-staged transport through a shared-memory file (shm_transport.cu): the
+// ranks are processes of one host, on one GPU or several.  Test harness of the
+// one-process-per-GPU engine path on a single B200 (NCCL refuses two ranks on
+// one device); no kernel ever waits on another process.
+Transport* make_shm_transport(const unsigned char id[128], int rank, int world);
 void nccl_unique_id(unsigned char id[128]);
 
 class EngineBase;
@@ -227,7 +235,9 @@ private:
     }
     static constexpr const char* tn() { return sizeof(T) == 4 ? "f32" : "f64"; }
     std::set<std::string> launched_;
-    void build_tensor_from_octant();
+    void init();
+    void release();
+    void build_tensor(const double* host_octant);
     void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr, bool skip_k1 = false,
                  bool fwd = false);
     // pass groups of one iteration: A = K1,K2 (slab -> send blocks), B = K3
@@ -236,6 +246,9 @@ private:
     void enq_B(const Iter& it, cudaEvent_t* ev = nullptr);
     void enq_C(const Iter& it, int cur, cudaEvent_t* ev = nullptr, bool fwd = false);
     void enq_local(const Iter& it, int cur);
+    void enq_K2(const Ctl& ctl, int comp0, int ncomp);
+    void enq_K3(const Ctl& ctl);
+    void enq_K4(const Ctl& ctl, int comp0, int ncomp);
     Ctl make_ctl(const Iter& it) const;
     StepIO make_io(const Iter& it) const;
     Halo<T> halo_ptrs() const;
@@ -263,6 +276,8 @@ private:
     Slab slab_;
     Transport* tr_ = nullptr;           // owned
     cudaStream_t stream_ = nullptr;
+    cudaStream_t cstream_ = nullptr;     // transposes / halo of a multi-process run
+    cudaEvent_t xev_[9] = {};            // fork / join events of the transpose pipeline
     T* M_[2] = {nullptr, nullptr};
     int cur_ = 0;
     T* H_ = nullptr;                     // H_eff / H_demag output
@@ -273,7 +288,6 @@ private:
     T* Kt_ = nullptr;
     C2<T>* tw_ = nullptr;
     int* ybuf_ = nullptr;
-    double* oct_ = nullptr;              // fp64 tensor octant [6][nz][ny][nx]
     int* err_ = nullptr;
     unsigned long long* torque_ = nullptr;
     double* sums_ = nullptr;             // [kMaxChunk][8]

@@ -91,6 +91,22 @@ template <class T>
 Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te, const mfd_stepper& st,
                   int device, Slab slab, Transport* tr)
     : grid_(g), mat_(m), terms_(te), st_(st), device_(device), slab_(slab), tr_(tr) {
+    // The engine owns tr and every buffer from the first statement on: a
+    // failure part-way releases them (the destructor does not run then).
+    try {
+        init();
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
+template <class T>
+void Engine<T>::init() {
+    const mfd_grid& g = grid_;
+    const mfd_terms& te = terms_;
+    const mfd_material& m = mat_;
+    const mfd_stepper& st = st_;
     precision = sizeof(T) == 4 ? 32 : 64;
     if (slab_.world <= 1) slab_ = Slab::of(g.nz, 0, 1);
     if (slab_.world > 1 && (g.nz % slab_.world != 0))
@@ -171,6 +187,12 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
     ck(cudaMallocHost((void**)&h_err_, sizeof(int)), "host alloc");
 
     if (G > 1) alloc(&halo_, 2 * 3 * (long long)g.nx * g.ny * sizeof(T));
+    if (G > 1 && tr_) {   // one process per GPU: transposes on a second stream (enqueue)
+        ck(cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking), "stream");
+        for (auto& e : xev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        tr_->reserve(terms_.demag ? (size_t)geo_.nz * g.ny * geo_.Hp * sizeof(C2<T>) : 0,
+                     (size_t)g.nx * g.ny * sizeof(T));
+    }
     if (terms_.demag) {
         const long long nrows = (long long)g.ny * nzl;
         (void)nrows;
@@ -254,12 +276,8 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
             }
             else if constexpr (z_variant<T, L>() == 0) set_smem<T>((const void*)k_fft_z_conv<T, L>, ZCfg<T, L>::SMEM);
         });
-        // tensor octant on the device (K0a, the whole global octant), then
-        // spectra (K0b) of this rank's x-bin block
-        alloc(&oct_, 6 * (long long)g.nx * g.ny * g.nz * sizeof(double));
-        launch_tensor_octant(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, oct_, stream_);
-        ck(cudaGetLastError(), "k_tensor_octant");
-        build_tensor_from_octant();
+        // tensor octant (K0a) and spectra (K0b) of this rank's x-bin block
+        build_tensor(nullptr);
     } else {
         k5_blocks_ = (n + 255) / 256;
     }
@@ -334,9 +352,16 @@ Engine<T>::Engine(const mfd_grid& g, const mfd_material& m, const mfd_terms& te,
 
 template <class T>
 Engine<T>::~Engine() {
+    release();
+}
+
+template <class T>
+void Engine<T>::release() {
     cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (cstream_) cudaStreamSynchronize(cstream_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, oct_, err_, torque_, sums_, partials_, ticket_, halo_};
+    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, err_, torque_, sums_, partials_, ticket_, halo_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (Ar_ && Ar_ != A_) cudaFree(Ar_);
@@ -346,77 +371,128 @@ Engine<T>::~Engine() {
     if (h_err_) cudaFreeHost(h_err_);
     if (h_perr_) cudaFreeHost(h_perr_);
     if (h_stage_) cudaFreeHost(h_stage_);
+    for (auto& e : xev_)
+        if (e) cudaEventDestroy(e);
+    if (cstream_) cudaStreamDestroy(cstream_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
-// K0b: separable cosine/sine transforms of the fp64 octant -> real spectrum octant in T.
+// K0a + K0b, rank-local and memory-bounded.  The fp64 octant (computed on the
+// device, or uploaded by the set_octant test hook) is produced a chunk of z
+// planes at a time, and each chunk goes straight through the x transform
+// restricted to this rank's x-bin block (Hv columns), so neither the full
+// octant (6 N doubles: 6.4 GB at 1024x1024x128) nor a full-width intermediate
+// is ever resident: per rank 6 x [nz][ny][Hv] + [nz][Hy][Hv] doubles plus one
+// <= 256 MB octant chunk, all freed before the first step.  Per output
+// element the GEMMs sum in the same order as a full-width transform, so every
+// rank's block is bitwise the single-GPU spectrum.  The spectra are separable
+// cos / sin transforms (the mirrored lattice has per-axis parity), so K~ comes
+// out real: only its octant Kt is stored (layout in step_kernels.cuh).
 template <class T>
-void Engine<T>::build_tensor_from_octant() {
+void Engine<T>::build_tensor(const double* host_oct) {
     const int nx = grid_.nx, ny = grid_.ny, nz = grid_.nz;   // global grid
-    const int Hx = geo_.Hx, Wb = geo_.Wb, u0 = geo_.ublk * geo_.Wb;
-    const long long n = (long long)nx * ny * nz;
-    double *Cx[2], *Cy[2], *Cz[2], *T1, *T2;
-    auto mat = [&](double** C, int H, int nn, int P) {
-        for (int odd = 0; odd < 2; ++odd) {
-            ck(cudaMalloc((void**)&C[odd], (size_t)H * nn * sizeof(double)), "cudaMalloc");
-            launch_axis_matrix(H, nn, P, odd, C[odd], stream_);
-        }
+    const int Hx = geo_.Hx, Wb = geo_.Wb, Hv = geo_.Hv, u0 = geo_.ublk * geo_.Wb;
+    ck(cudaMemsetAsync(Kt_, 0, 6 * (long long)Hy_ * Hz_ * Wb * sizeof(T), stream_), "memset");
+    if (Hv <= 0) {
+        ck(cudaStreamSynchronize(stream_), "tensor setup");
+        return;
+    }
+    const long long plane = (long long)nx * ny, n = plane * nz;
+    const int KC = (int)std::max<long long>(1, std::min<long long>(nz, (256LL << 20) / (6 * plane * 8)));
+    std::vector<void*> tmp;
+    auto dalloc = [&](size_t bytes) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, bytes), "cudaMalloc (tensor setup)");
+        tmp.push_back(p);
+        return (double*)p;
     };
-    mat(Cx, Hx, nx, geo_.Px);
-    mat(Cy, Hy_, ny, Py_);
-    mat(Cz, Hz_, nz, Pz_);
-    ck(cudaMalloc((void**)&T1, (size_t)nz * ny * Hx * sizeof(double)), "cudaMalloc");
-    ck(cudaMalloc((void**)&T2, (size_t)nz * Hy_ * Hx * sizeof(double)), "cudaMalloc");
-    // parity per component (xx,yy,zz,xy,xz,yz): odd along x / y / z
-    const int ox[6] = {0, 0, 0, 1, 1, 0}, oy[6] = {0, 0, 0, 1, 0, 1}, oz[6] = {0, 0, 0, 0, 1, 1};
-    for (int c = 0; c < 6; ++c) {
-        GemmDesc d{};
-        // x: T1[row][u] = sum_i E[row][i] Cx[u][i]
-        d = GemmDesc{};
-        d.Mdim = ny * nz; d.Ndim = Hx; d.Kdim = nx;
-        d.a_m = nx; d.a_k = 1; d.b_k = 1; d.b_n = nx; d.o_m = Hx; d.o_n = 1; d.nb2 = 1; d.scale = 1.0;
-        launch_gemm64(d, 1, oct_ + c * n, Cx[ox[c]], T1, stream_);
-        // y: T2[k][v][u] = sum_j Cy[v][j] T1[k][j][u]
-        d = GemmDesc{};
-        d.Mdim = Hy_; d.Ndim = Hx; d.Kdim = ny;
-        d.a_m = ny; d.a_k = 1; d.b_k = Hx; d.b_n = 1; d.o_m = Hx; d.o_n = 1;
-        d.b_b1 = (long long)ny * Hx; d.o_b1 = (long long)Hy_ * Hx; d.nb2 = 1; d.scale = 1.0;
-        launch_gemm64(d, nz, Cy[oy[c]], T1, T2, stream_);
-        // z: Kt[v][w][u][c] = s * sum_k Cz[w][k] T2[k][v][u0+u] for this rank's x-bin block;
-        // two odd axes give (-2i)^2 = -4 -> s = -1.  The six components of a
-        // bin are interleaved so K3 reads them as three vectors.
-        if (geo_.Hv > 0) {
-            d = GemmDesc{};
-            d.Mdim = Hz_; d.Ndim = geo_.Hv; d.Kdim = nz;
-            d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hx; d.b_n = 1; d.o_m = 6LL * Wb; d.o_n = 6;
-            d.b_b1 = Hx; d.o_b1 = 6LL * Hz_ * Wb; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
-            launch_gemm64(d, Hy_, Cz[oz[c]], T2 + u0, Kt_ + c, stream_);
+    try {
+        double *Cx[2], *Cy[2], *Cz[2];
+        auto mat = [&](double** C, int H, int nn, int P) {
+            for (int odd = 0; odd < 2; ++odd) {
+                C[odd] = dalloc((size_t)H * nn * sizeof(double));
+                launch_axis_matrix(H, nn, P, odd, C[odd], stream_);
+            }
+        };
+        mat(Cx, Hx, nx, geo_.Px);
+        mat(Cy, Hy_, ny, Py_);
+        mat(Cz, Hz_, nz, Pz_);
+        double* Ech = dalloc((size_t)6 * KC * plane * sizeof(double));
+        const long long t1c = (long long)nz * ny * Hv;               // T1 component stride
+        double* T1 = dalloc((size_t)6 * t1c * sizeof(double));
+        double* T2 = dalloc((size_t)nz * Hy_ * Hv * sizeof(double));
+        // parity per component (xx,yy,zz,xy,xz,yz): odd along x / y / z
+        const int ox[6] = {0, 0, 0, 1, 1, 0}, oy[6] = {0, 0, 0, 1, 0, 1}, oz[6] = {0, 0, 0, 0, 1, 1};
+        for (int kb = 0; kb < nz; kb += KC) {
+            const int kc = std::min(KC, nz - kb);
+            const long long cs = (long long)kc * plane;               // chunk component stride
+            if (host_oct) {
+                for (int c = 0; c < 6; ++c)
+                    ck(cudaMemcpyAsync(Ech + c * cs, host_oct + c * n + kb * plane, cs * sizeof(double),
+                                       cudaMemcpyHostToDevice, stream_), "octant upload");
+            } else {
+                launch_tensor_octant(nx, ny, kb, kc, grid_.dx, grid_.dy, grid_.dz, Ech, stream_);
+                ck(cudaGetLastError(), "k_tensor_octant");
+            }
+            for (int c = 0; c < 6; ++c) {
+                // x: T1[k][j][u] = sum_i E[k][j][i] Cx[u0+u][i], u < Hv
+                GemmDesc d{};
+                d.Mdim = kc * ny; d.Ndim = Hv; d.Kdim = nx;
+                d.a_m = nx; d.a_k = 1; d.b_k = 1; d.b_n = nx; d.o_m = Hv; d.o_n = 1; d.nb2 = 1; d.scale = 1.0;
+                launch_gemm64(d, 1, Ech + c * cs, Cx[ox[c]] + (long long)u0 * nx, T1 + c * t1c + (long long)kb * ny * Hv,
+                              stream_);
+            }
+            ck(cudaGetLastError(), "tensor gemm");
+            if (host_oct) ck(cudaStreamSynchronize(stream_), "octant upload");   // pageable source
         }
-        ck(cudaGetLastError(), "tensor gemm");
+        for (int c = 0; c < 6; ++c) {
+            // y: T2[k][v][u] = sum_j Cy[v][j] T1[k][j][u]
+            GemmDesc d{};
+            d.Mdim = Hy_; d.Ndim = Hv; d.Kdim = ny;
+            d.a_m = ny; d.a_k = 1; d.b_k = Hv; d.b_n = 1; d.o_m = Hv; d.o_n = 1;
+            d.b_b1 = (long long)ny * Hv; d.o_b1 = (long long)Hy_ * Hv; d.nb2 = 1; d.scale = 1.0;
+            launch_gemm64(d, nz, Cy[oy[c]], T1 + c * t1c, T2, stream_);
+            // z: Kt[v][w][u][c] = s * sum_k Cz[w][k] T2[k][v][u]; two odd axes give
+            // (-2i)^2 = -4 -> s = -1.  The six components of a bin are interleaved
+            // so K3 reads them as three vectors.
+            d = GemmDesc{};
+            d.Mdim = Hz_; d.Ndim = Hv; d.Kdim = nz;
+            d.a_m = nz; d.a_k = 1; d.b_k = (long long)Hy_ * Hv; d.b_n = 1; d.o_m = 6LL * Wb; d.o_n = 6;
+            d.b_b1 = Hv; d.o_b1 = 6LL * Hz_ * Wb; d.nb2 = 1; d.scale = c >= 3 ? -1.0 : 1.0;
+            launch_gemm64(d, Hy_, Cz[oz[c]], T2, Kt_ + c, stream_);
+            ck(cudaGetLastError(), "tensor gemm");
+        }
+        ck(cudaStreamSynchronize(stream_), "tensor setup");
+    } catch (...) {
+        cudaStreamSynchronize(stream_);
+        for (void* p : tmp) cudaFree(p);
+        throw;
     }
-    ck(cudaStreamSynchronize(stream_), "tensor setup");
-    for (int odd = 0; odd < 2; ++odd) {
-        cudaFree(Cx[odd]);
-        cudaFree(Cy[odd]);
-        cudaFree(Cz[odd]);
-    }
-    cudaFree(T1);
-    cudaFree(T2);
+    for (void* p : tmp) cudaFree(p);
 }
 
 template <class T>
 void Engine<T>::set_octant(const double* oct) {
     if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
-    ck(cudaMemcpy(oct_, oct, 6 * (long long)grid_.nx * grid_.ny * grid_.nz * sizeof(double), cudaMemcpyHostToDevice),
-       "octant upload");
-    build_tensor_from_octant();
+    build_tensor(oct);
 }
 
+// Test hook: the device octant is transient (freed after setup), so it is
+// recomputed here for the caller.
 template <class T>
 void Engine<T>::get_octant(double* oct) {
     if (!terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
-    ck(cudaMemcpy(oct, oct_, 6 * (long long)grid_.nx * grid_.ny * grid_.nz * sizeof(double), cudaMemcpyDeviceToHost),
-       "octant download");
+    const long long n = 6LL * grid_.nx * grid_.ny * grid_.nz;
+    double* d = nullptr;
+    ck(cudaMalloc((void**)&d, n * sizeof(double)), "cudaMalloc");
+    launch_tensor_octant(grid_.nx, grid_.ny, 0, grid_.nz, grid_.dx, grid_.dy, grid_.dz, d, stream_);
+    const cudaError_t e1 = cudaGetLastError();
+    const cudaError_t e2 = cudaMemcpyAsync(oct, d, n * sizeof(double), cudaMemcpyDeviceToHost, stream_);
+    const cudaError_t e3 = cudaStreamSynchronize(stream_);
+    cudaFree(d);
+    ck(e1, "k_tensor_octant");
+    ck(e2, "octant download");
+    ck(e3, "octant download");
 }
 
 template <class T>
@@ -519,31 +595,49 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
         if (ev) for (int q = 2; q <= 4; ++q) ck(cudaEventRecordWithFlags(ev[q], stream_, cudaEventRecordExternal), "event");
         return;
     }
-    const bool work = geo_.Hv > 0;
-    if (work && k2_tma_) {
+    enq_K2(ctl, 0, 3);
+    if (ev) ck(cudaEventRecordWithFlags(ev[2], stream_, cudaEventRecordExternal), "event");
+    if (stop_after_ == 2) return;
+    enq_K3(ctl);
+    if (ev) ck(cudaEventRecordWithFlags(ev[3], stream_, cudaEventRecordExternal), "event");
+    if (stop_after_ == 3) return;
+    enq_K4(ctl, 0, 3);
+    if (ev) ck(cudaEventRecordWithFlags(ev[4], stream_, cudaEventRecordExternal), "event");
+}
+
+// K2 (y forward) of components [comp0, comp0 + ncomp): Ar_ -> B_
+template <class T>
+void Engine<T>::enq_K2(const Ctl& ctl, int comp0, int ncomp) {
+    if (geo_.Hv <= 0) return;
+    if (k2_tma_) {
         with_pow2(Py_, [&]<int L>() {
             if constexpr (YTCfg<T, L>::OK) {
                 using CF = YTCfg<T, L>;
                 const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
                 auto* k = 2 * geo_.ny == L ? k_fft_y_fwd_tma<T, L, true> : k_fft_y_fwd_tma<T, L, false>;
                 note("K2 k_fft_y_fwd_tma<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
-                k<<<k2_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmA_, B_, tw_, ctl, ntx, k2_box_);
+                const int grid = (int)std::min<long long>(k2_grid_, (long long)ntx * geo_.nzg * ncomp);
+                k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, tmA_, B_, tw_, ctl, ntx, k2_box_, comp0, ncomp);
             }
         });
-    } else if (work) {
+    } else {
         with_pow2(Py_, [&]<int L>() {
             using CF = YCfg<T, L>;
-            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+            dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, ncomp);
             note("K2 k_fft_y_fwd<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
             if (2 * geo_.ny == L)
-                k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
+                k_fft_y_fwd<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl, comp0);
             else
-                k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl);
+                k_fft_y_fwd<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, Ar_, B_, tw_, ctl, comp0);
         });
     }
-    if (ev) ck(cudaEventRecordWithFlags(ev[2], stream_, cudaEventRecordExternal), "event");
-    if (stop_after_ == 2) return;
-    if (work) with_pow2(Pz_, [&]<int L>() {
+}
+
+// K3 (z transform, tensor product, inverse z) on B_, all components
+template <class T>
+void Engine<T>::enq_K3(const Ctl& ctl) {
+    if (geo_.Hv <= 0) return;
+    with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
             dim3 grid((geo_.Hv + 31) / 32, Hy_, 1);
             note("K3 k_fft_z_conv1<%s,%d>", tn(), L);
@@ -569,27 +663,31 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
             k_fft_z_conv<T, L><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Kt_, tw_, ybuf_, ctl);
         }
     });
-    if (ev) ck(cudaEventRecordWithFlags(ev[3], stream_, cudaEventRecordExternal), "event");
-    if (stop_after_ == 3) return;
-    if (work && k4_tma_) with_pow2(Py_, [&]<int L>() {
+}
+
+// K4 (y inverse) of components [comp0, comp0 + ncomp): B_ -> Ar_
+template <class T>
+void Engine<T>::enq_K4(const Ctl& ctl, int comp0, int ncomp) {
+    if (geo_.Hv <= 0) return;
+    if (k4_tma_) with_pow2(Py_, [&]<int L>() {
         if constexpr (YICfg<T, L>::OK) {
             using CF = YICfg<T, L>;
             const int ntx = (geo_.Hv + CF::W - 1) / CF::W;
             auto* k = 2 * geo_.ny == L ? k_fft_y_inv_tma<T, L, true> : k_fft_y_inv_tma<T, L, false>;
             note("K4 k_fft_y_inv_tma<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
-            k<<<k4_grid_, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, Ar_, tw_, ctl, ntx);
+            const int grid = (int)std::min<long long>(k4_grid_, (long long)ntx * geo_.nzg * ncomp);
+            k<<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, tmB_, Ar_, tw_, ctl, ntx, comp0, ncomp);
         }
     });
-    else if (work) with_pow2(Py_, [&]<int L>() {
+    else with_pow2(Py_, [&]<int L>() {
         using CF = YCfg<T, L>;
-        dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, 3);
+        dim3 grid((geo_.Hv + CF::W - 1) / CF::W, geo_.nzg, ncomp);
         note("K4 k_fft_y_inv<%s,%d,FY=%d>", tn(), L, (int)(2 * geo_.ny == L));
         if (2 * geo_.ny == L)
-            k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
+            k_fft_y_inv<T, L, true><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl, comp0);
         else
-            k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl);
+            k_fft_y_inv<T, L, false><<<grid, CF::NT, CF::SMEM, stream_>>>(geo_, B_, Ar_, tw_, ctl, comp0);
     });
-    if (ev) ck(cudaEventRecordWithFlags(ev[4], stream_, cudaEventRecordExternal), "event");
 }
 
 // C: K5 (x inverse + H_eff + LLG + Euler) on A_ (the receive side of the second transpose)
@@ -636,33 +734,71 @@ void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
     });
 }
 
-// One iteration.  Multi-GPU (tr_ set): M halo, the two all-to-all transposes
-// around K3 and the scalar allreduces are issued on the same stream, so they
-// are captured into the step graph with the kernels.
+// One iteration.  Multi-GPU (tr_ set): the M halo, the two all-to-all
+// transposes and the scalar allreduces are enqueued like the kernels, so they
+// are captured into the step graph.  The transposes run per component on a
+// second stream (cstream_) and overlap the y passes:
+// all-to-all #1 of component c+1 flies while K2 transforms component c, and
+// all-to-all #2 of component c while K4 transforms c+1; the halo (needed only
+// by K5) flies during K1-K4.  The passes themselves are the single-GPU ones.
 template <class T>
 void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, bool skip_k1, bool fwd) {
     const size_t tsz = sizeof(T);
+    const bool multi = tr_ && slab_.world > 1;
     if (events) ck(cudaEventRecordWithFlags(ev[0], stream_, cudaEventRecordExternal), "event");
-    if (tr_ && slab_.world > 1)
+    if (multi) {   // fork: the comm stream joins everything enqueued so far
+        ck(cudaEventRecord(xev_[0], stream_), "event");
+        ck(cudaStreamWaitEvent(cstream_, xev_[0], 0), "wait");
         tr_->halo(M_[cur], geo_.ncell * tsz, (size_t)grid_.nx * grid_.ny * tsz, geo_.nz, halo_,
-                  halo_ + 3LL * grid_.nx * grid_.ny, stream_);
+                  halo_ + 3LL * grid_.nx * grid_.ny, cstream_);
+    }
     if (!terms_.demag) {
+        if (multi) {   // join before the stencil
+            ck(cudaEventRecord(xev_[1], cstream_), "event");
+            ck(cudaStreamWaitEvent(stream_, xev_[1], 0), "wait");
+        }
         enq_local(it, cur);
         if (events)
             for (int q = 1; q < 6; ++q) ck(cudaEventRecordWithFlags(ev[q], stream_, cudaEventRecordExternal), "event");
-    } else {
+    } else if (!multi) {
         enq_A(it, cur, events ? ev : nullptr, skip_k1);
         if (stop_after_ == 1) return;
-        // transpose #1: x-bin block p of every local plane -> rank p
-        if (tr_ && slab_.world > 1) tr_->alltoall(A_, Ar_, geo_.SA * sizeof(C2<T>), stream_);
         enq_B(it, events ? ev : nullptr);
         if (stop_after_ >= 2 && stop_after_ <= 4) return;
-        // transpose #2 (inverse): back to this rank's planes, all x-bins
-        if (tr_ && slab_.world > 1) tr_->alltoall(Ar_, A_, geo_.SA * sizeof(C2<T>), stream_);
         enq_C(it, cur, events ? ev : nullptr, fwd);
         if (events) ck(cudaEventRecordWithFlags(ev[5], stream_, cudaEventRecordExternal), "event");
+    } else {
+        const Ctl ctl = make_ctl(it);
+        // component c of x-bin block p sits at p * SA + c * cblk (contiguous)
+        const size_t cblk = (size_t)geo_.nz * geo_.ny * geo_.Hp, stride = (size_t)geo_.SA * sizeof(C2<T>);
+        const size_t cbytes = cblk * sizeof(C2<T>);
+        enq_A(it, cur, events ? ev : nullptr, false);
+        ck(cudaEventRecord(xev_[1], stream_), "event");
+        ck(cudaStreamWaitEvent(cstream_, xev_[1], 0), "wait");
+        for (int c = 0; c < 3; ++c) {   // transpose #1: x-bin block p of every local plane -> rank p
+            tr_->alltoall(A_ + c * cblk, Ar_ + c * cblk, cbytes, stride, cstream_);
+            ck(cudaEventRecord(xev_[2 + c], cstream_), "event");
+        }
+        for (int c = 0; c < 3; ++c) {
+            ck(cudaStreamWaitEvent(stream_, xev_[2 + c], 0), "wait");
+            enq_K2(ctl, c, 1);
+        }
+        if (events) ck(cudaEventRecordWithFlags(ev[2], stream_, cudaEventRecordExternal), "event");
+        enq_K3(ctl);
+        if (events) ck(cudaEventRecordWithFlags(ev[3], stream_, cudaEventRecordExternal), "event");
+        for (int c = 0; c < 3; ++c) {   // transpose #2 (inverse): back to this rank's planes, all x-bins
+            enq_K4(ctl, c, 1);
+            ck(cudaEventRecord(xev_[5 + c], stream_), "event");
+            ck(cudaStreamWaitEvent(cstream_, xev_[5 + c], 0), "wait");
+            tr_->alltoall(Ar_ + c * cblk, A_ + c * cblk, cbytes, stride, cstream_);
+        }
+        if (events) ck(cudaEventRecordWithFlags(ev[4], stream_, cudaEventRecordExternal), "event");
+        ck(cudaEventRecord(xev_[8], cstream_), "event");   // join (also covers the halo)
+        ck(cudaStreamWaitEvent(stream_, xev_[8], 0), "wait");
+        enq_C(it, cur, events ? ev : nullptr, false);
+        if (events) ck(cudaEventRecordWithFlags(ev[5], stream_, cudaEventRecordExternal), "event");
     }
-    if (tr_ && slab_.world > 1) {
+    if (multi) {
         tr_->allreduce_max_u64(torque_ + it.slot, 1, stream_);
         tr_->allreduce_max_i32(err_, 1, stream_);
         if (it.sums) tr_->allreduce_sum_f64(sums_ + 8 * it.slot, 7, stream_);

@@ -31,11 +31,11 @@ public:
     ~NcclTransport() override {
         if (comm_) ncclCommDestroy(comm_);
     }
-    void alltoall(const void* send, void* recv, size_t blk, cudaStream_t s) override {
+    void alltoall(const void* send, void* recv, size_t blk, size_t stride, cudaStream_t s) override {
         nk(ncclGroupStart(), "ncclGroupStart");
         for (int p = 0; p < world_; ++p) {
-            const char* sp = static_cast<const char*>(send) + p * blk;
-            char* rp = static_cast<char*>(recv) + p * blk;
+            const char* sp = static_cast<const char*>(send) + p * stride;
+            char* rp = static_cast<char*>(recv) + p * stride;
             if (p == rank_) {
                 ck(cudaMemcpyAsync(rp, sp, blk, cudaMemcpyDeviceToDevice, s), "self block");
                 continue;

@@ -419,14 +419,15 @@ k_r2c_x_pipe(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>*
 // pruned first stage never meets a row >= ny and the row test disappears.
 template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB_FWD)
-k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl) {
+k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<T>* __restrict__ tw, Ctl ctl,
+            int comp0) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
     if (halted_mid(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
-    const int k = blockIdx.y, comp = blockIdx.z;   // k: global plane
+    const int k = blockIdx.y, comp = comp0 + (int)blockIdx.z;   // k: global plane
     const C2<T>* src = A + arow_y(g, comp, k, 0) + u0;
     C2<T>* dst = B + comp * g.S_c + k * g.S_k + u0;
     const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
@@ -458,7 +459,7 @@ template <class T, int L> struct YTCfg {
 template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YTCfg<T, L>::NT, 2)
 k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restrict__ B,
-                const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int box_rows) {
+                const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int box_rows, int comp0, int ncomp) {
     using CF = YTCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
     constexpr int TWL = kK2StridedTw ? TWN : L;
@@ -469,7 +470,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     C2<T>* stage = align128(work + W * L);
     __shared__ uint64_t bar;
     const int ny = g.ny, nz = g.nzg, Wb = g.Wb;   // all planes of this rank's x-bin block
-    const int ntiles = ntx * nz * 3;
+    const int ntiles = ntx * nz * ncomp;          // components [comp0, comp0 + ncomp)
     int t = blockIdx.x;
     if (t >= ntiles) return;
     if (threadIdx.x == 0) {
@@ -479,7 +480,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     }
     __syncthreads();
     auto issue = [&](int tt) {   // one thread
-        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
+        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = comp0 + tt / (ntx * nz);
         const int kb = k / g.nz, kl = k - kb * g.nz;   // plane k came from rank kb
         const int row0 = ((kb * 3 + comp) * g.nz + kl) * ny;
         mbar_arrive_expect_tx(&bar, (unsigned)(ny * W * CF::CS));
@@ -496,7 +497,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     };
 #pragma unroll 1
     for (; t < ntiles; t += gridDim.x) {
-        const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
+        const int bx = t % ntx, k = (t / ntx) % nz, comp = comp0 + t / (ntx * nz);
         const int u0 = bx * W;
         C2<T>* dst = B + comp * g.S_c + k * g.S_k + u0;
         auto stn = [&](int col, int pos, C2<T> v) { dst[pos * Wb + col] = v; };
@@ -516,14 +517,15 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
 // ------------------------------------------------------------------ K4
 template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YCfg<T, L>::NT, YCfg<T, L>::MINB_INV)
-k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl,
+            int comp0) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
     if (halted_mid(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
-    const int k = blockIdx.y, comp = blockIdx.z;   // k: global plane
+    const int k = blockIdx.y, comp = comp0 + (int)blockIdx.z;   // k: global plane
     const C2<T>* src = B + comp * g.S_c + k * g.S_k + u0;
     C2<T>* dst = A + arow_y(g, comp, k, 0) + u0;
     const int ny = g.ny, Hp = g.Hp, Wb = g.Wb;
@@ -565,7 +567,7 @@ template <class T, int L> struct YICfg {
 template <class T, int L, bool FY>
 __global__ void __launch_bounds__(YICfg<T, L>::NT, YICfg<T, L>::MINB)
 k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restrict__ A,
-                const C2<T>* __restrict__ tw, Ctl ctl, int ntx) {
+                const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int comp0, int ncomp) {
     using CF = YICfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT, R0 = CF::R0, R1 = CF::R1, HALF = CF::HALF;
     if (halted_mid(ctl)) return;
@@ -573,13 +575,13 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
     C2<T>* slot0 = align128(reinterpret_cast<C2<T>*>(smem_raw));
     __shared__ uint64_t bar[3];
     const int ny = g.ny, nz = g.nzg, Hp = g.Hp;   // all planes of this rank's x-bin block
-    const int ntiles = ntx * nz * 3;
+    const int ntiles = ntx * nz * ncomp;          // components [comp0, comp0 + ncomp)
     if ((int)blockIdx.x >= ntiles) return;
     // fill f = 2 i + h (tile i of this CTA, half h) -> slot f % 3, phase (f / 3) & 1
     auto issue = [&](int i, int h) {   // one thread
         const int tt = blockIdx.x + i * gridDim.x;
         if (tt >= ntiles) return;
-        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = tt / (ntx * nz);
+        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = comp0 + tt / (ntx * nz);
         const int u0 = bx * W;
         const int row0 = (comp * nz + k) * L + h * CF::HALF;
         const int s = (2 * i + h) % 3;
@@ -598,7 +600,7 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
     for (int i = 0;; ++i) {
         const int t = blockIdx.x + i * gridDim.x;
         if (t >= ntiles) break;
-        const int bx = t % ntx, k = (t / ntx) % nz, comp = t / (ntx * nz);
+        const int bx = t % ntx, k = (t / ntx) % nz, comp = comp0 + t / (ntx * nz);
         const int u0 = bx * W;
         C2<T>* sa = slot0 + ((2 * i) % 3) * CF::SLOTE;
         C2<T>* sb = slot0 + ((2 * i + 1) % 3) * CF::SLOTE;

@@ -4,9 +4,10 @@
 
 namespace mfd {
 
-void launch_tensor_octant(int nx, int ny, int nz, double dx, double dy, double dz, double* out, cudaStream_t s) {
-    const long long n = (long long)nx * ny * nz;
-    k_tensor_octant<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(nx, ny, nz, dx, dy, dz, out);
+void launch_tensor_octant(int nx, int ny, int k0, int nzc, double dx, double dy, double dz, double* out,
+                          cudaStream_t s) {
+    const long long n = (long long)nx * ny * nzc;
+    if (n > 0) k_tensor_octant<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(nx, ny, k0, nzc, dx, dy, dz, out);
 }
 void launch_axis_matrix(int H, int n, int P, int odd, double* C, cudaStream_t s) {
     k_axis_matrix<<<(unsigned)(((long long)H * n + 255) / 256), 256, 0, s>>>(H, n, P, odd, C);

@@ -265,11 +265,13 @@ __device__ __host__ inline int far_order(int di, int dj, int dk, double a, doubl
 }
 
 // K0a: one thread per octant entry; out layout [6][nz][ny][nx] (fp64).
-__global__ void k_tensor_octant(int nx, int ny, int nz, double a, double b, double c, double* __restrict__ out) {
-    const long long n = (long long)nx * ny * nz;
+// Planes [k0, k0 + nzc) of the octant; out = [6][nzc][ny][nx].
+__global__ void k_tensor_octant(int nx, int ny, int k0, int nzc, double a, double b, double c,
+                                double* __restrict__ out) {
+    const long long n = (long long)nx * ny * nzc;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
-    const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = (int)(e / ((long long)nx * ny));
+    const int i = (int)(e % nx), j = (int)((e / nx) % ny), k = k0 + (int)(e / ((long long)nx * ny));
     const double X = i * a, Y = j * b, Z = k * c;
     double K6[6];
     const int ord = far_order(i, j, k, a, b, c);

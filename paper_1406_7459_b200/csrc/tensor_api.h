@@ -12,8 +12,9 @@ struct GemmDesc {
     double scale;
 };
 
-// K0a: K = -N octant [6][nz][ny][nx] (fp64).
-void launch_tensor_octant(int nx, int ny, int nz, double dx, double dy, double dz, double* out, cudaStream_t s);
+// K0a: K = -N octant planes [k0, k0 + nzc): out = [6][nzc][ny][nx] (fp64).
+void launch_tensor_octant(int nx, int ny, int k0, int nzc, double dx, double dy, double dz, double* out,
+                          cudaStream_t s);
 // Transform matrix [H][n] (cos with weights 1,2,2,.. or 2 sin).
 void launch_axis_matrix(int H, int n, int P, int odd, double* C, cudaStream_t s);
 // K0b batched fp64 GEMM, output fp64 or fp32.
