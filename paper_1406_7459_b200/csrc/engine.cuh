@@ -4,6 +4,7 @@
 // (sim.hpp:33-62, dynamics.hpp:157-198).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -26,6 +27,18 @@ namespace mfd {
 struct Error : std::runtime_error {
     mfd_status code;
     Error(mfd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// NVTX range (header-only NVTX v3: free unless a profiler injects a tool).
+// The per-pass ranges carry the reference's StepTiming phase names
+// (backend.hpp:147-148); inside a CUDA graph they mark the capture, and the
+// eager / instrumented paths (mfd_last_step_timing) and the chunk launches
+// show them at run time.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
 };
 
 inline void ck(cudaError_t e, const char* what) {

@@ -390,6 +390,7 @@ void Engine<T>::release() {
 // out real: only its octant Kt is stored (layout in step_kernels.cuh).
 template <class T>
 void Engine<T>::build_tensor(const double* host_oct) {
+    Nvtx r("setup: demag tensor + spectra (K0a/K0b)");
     const int nx = grid_.nx, ny = grid_.ny, nz = grid_.nz;   // global grid
     const int Hx = geo_.Hx, Wb = geo_.Wb, Hv = geo_.Hv, u0 = geo_.ublk * geo_.Wb;
     ck(cudaMemsetAsync(Kt_, 0, 6 * (long long)Hy_ * Hz_ * Wb * sizeof(T), stream_), "memset");
@@ -544,6 +545,7 @@ Halo<T> Engine<T>::halo_ptrs() const {
 
 template <class T>
 void Engine<T>::enq_local(const Iter& it, int cur) {
+    Nvtx r("localFields + integrate");
     note("K5 k_local_llg<%s>", tn());
     k_local_llg<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
         geo_, M_[cur], M_[cur ^ 1], H_, lp_, make_io(it), make_ctl(it), halo_ptrs());
@@ -552,6 +554,7 @@ void Engine<T>::enq_local(const Iter& it, int cur) {
 // A: K1 (x, R2C) -> A_ (on several GPUs: the send blocks, one per rank's x-bins)
 template <class T>
 void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
+    Nvtx r("pad+forwardFft x (K1)");
     const Ctl ctl = make_ctl(it);
     const long long nrows = (long long)geo_.ny * geo_.nz;
     if (!skip_k1) with_pow2(geo_.N, [&]<int L>() {
@@ -608,6 +611,7 @@ void Engine<T>::enq_B(const Iter& it, cudaEvent_t* ev) {
 // K2 (y forward) of components [comp0, comp0 + ncomp): Ar_ -> B_
 template <class T>
 void Engine<T>::enq_K2(const Ctl& ctl, int comp0, int ncomp) {
+    Nvtx r("forwardFft y (K2)");
     if (geo_.Hv <= 0) return;
     if (k2_tma_) {
         with_pow2(Py_, [&]<int L>() {
@@ -636,6 +640,7 @@ void Engine<T>::enq_K2(const Ctl& ctl, int comp0, int ncomp) {
 // K3 (z transform, tensor product, inverse z) on B_, all components
 template <class T>
 void Engine<T>::enq_K3(const Ctl& ctl) {
+    Nvtx r("forwardFft z + spectralMultiply + inverseFft z (K3)");
     if (geo_.Hv <= 0) return;
     with_pow2(Pz_, [&]<int L>() {
         if constexpr (z_variant<T, L>() == 1) {
@@ -668,6 +673,7 @@ void Engine<T>::enq_K3(const Ctl& ctl) {
 // K4 (y inverse) of components [comp0, comp0 + ncomp): B_ -> Ar_
 template <class T>
 void Engine<T>::enq_K4(const Ctl& ctl, int comp0, int ncomp) {
+    Nvtx r("inverseFft y (K4)");
     if (geo_.Hv <= 0) return;
     if (k4_tma_) with_pow2(Py_, [&]<int L>() {
         if constexpr (YICfg<T, L>::OK) {
@@ -693,6 +699,7 @@ void Engine<T>::enq_K4(const Ctl& ctl, int comp0, int ncomp) {
 // C: K5 (x inverse + H_eff + LLG + Euler) on A_ (the receive side of the second transpose)
 template <class T>
 void Engine<T>::enq_C(const Iter& it, int cur, cudaEvent_t* ev, bool fwd) {
+    Nvtx r("inverseFft x + localFields + integrate (K5)");
     const Ctl ctl = make_ctl(it);
     const StepIO io = make_io(it);
     const Halo<T> hl = halo_ptrs();
@@ -776,6 +783,7 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, b
         ck(cudaEventRecord(xev_[1], stream_), "event");
         ck(cudaStreamWaitEvent(cstream_, xev_[1], 0), "wait");
         for (int c = 0; c < 3; ++c) {   // transpose #1: x-bin block p of every local plane -> rank p
+            Nvtx r("transpose #1 (all-to-all, x-spectrum)");
             tr_->alltoall(A_ + c * cblk, Ar_ + c * cblk, cbytes, stride, cstream_);
             ck(cudaEventRecord(xev_[2 + c], cstream_), "event");
         }
@@ -790,6 +798,7 @@ void Engine<T>::enqueue(const Iter& it, int cur, bool events, cudaEvent_t* ev, b
             enq_K4(ctl, c, 1);
             ck(cudaEventRecord(xev_[5 + c], stream_), "event");
             ck(cudaStreamWaitEvent(cstream_, xev_[5 + c], 0), "wait");
+            Nvtx r("transpose #2 (all-to-all, x-spectrum)");
             tr_->alltoall(Ar_ + c * cblk, A_ + c * cblk, cbytes, stride, cstream_);
         }
         if (events) ck(cudaEventRecordWithFlags(ev[4], stream_, cudaEventRecordExternal), "event");
@@ -856,6 +865,7 @@ cudaGraphExec_t Engine<T>::chunk_graph(const std::vector<Iter>& its, int cur) {
 // Launch a chunk of iterations.
 template <class T>
 void Engine<T>::run_chunk(const std::vector<Iter>& its, int cur) {
+    Nvtx r("step chunk (graph launch)");
     ck(cudaGraphLaunch(chunk_graph(its, cur), stream_), "graph launch");
 }
 
