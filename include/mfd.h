@@ -126,6 +126,14 @@ mfd_status mfd_get_time(const mfd_ctx* ctx, double* t, long* step);
 
 mfd_status mfd_effective_field_f64(mfd_ctx* ctx, double* hx, double* hy, double* hz);
 mfd_status mfd_demag_field_f64(mfd_ctx* ctx, double* hx, double* hy, double* hz);
+/* The same in float (the f32 engine copies its fields out unconverted). */
+mfd_status mfd_effective_field_f32(mfd_ctx* ctx, float* hx, float* hy, float* hz);
+mfd_status mfd_demag_field_f32(mfd_ctx* ctx, float* hx, float* hy, float* hz);
+
+/* Replace the StepperConfig (dt, renormalizeEvery, maxSteps, torque tolerance,
+ * sampleEvery) of a live context (dynamics::relax takes its config per call,
+ * dynamics.hpp:157-160); validation as StepperConfig::validate (dynamics.hpp:26-30). */
+mfd_status mfd_set_stepper(mfd_ctx* ctx, const mfd_stepper* stepper);
 
 /* nsteps x Simulation::step; *last_torque = pre-step max torque (deg/ns) of the last
  * step; torques (optional, nsteps entries) receives every step's value. */
@@ -139,8 +147,9 @@ mfd_status mfd_sample_now(mfd_ctx* ctx, mfd_sample* out);
 mfd_status mfd_reduced_mean(mfd_ctx* ctx, double m[3]);
 mfd_status mfd_energies(mfd_ctx* ctx, double e[5]);
 
-/* Device time of the phases of one instrumented step, ms:
- * [pad+forward x, forward y, z + multiply, inverse y, inverse x + local + integrate, total, 0]. */
+/* One real Simulation::step, instrumented: device time of its passes, ms, and its torque:
+ * [pad+forward x, forward y, z + multiply, inverse y, inverse x + local + integrate, total,
+ *  pre-step max torque in deg/ns]. */
 mfd_status mfd_last_step_timing(mfd_ctx* ctx, double ms[7]);
 
 /* Stability heuristic (dynamics.hpp:39-45). */
@@ -180,6 +189,10 @@ double mfd_model_bytes_per_step(const mfd_ctx* ctx);
  * line ("K5 k_c2r_x_llg_v<f32,256,SUMS=0,RS=0,FWD=1,MULTI=0>", ...).  Copies at most
  * len-1 bytes + NUL into buf (may be NULL) and returns the full length + 1. */
 int mfd_debug_variants(const mfd_ctx* ctx, char* buf, int len);
+/* With MFD_GUARD=1 in the environment at mfd_create, every device buffer is bracketed by
+ * 4 KB guard bands of 0xA5; returns the number of guard bytes overwritten so far
+ * (-1: guards off, -2: error).  A write-overrun check for the tests. */
+long long mfd_debug_guard_check(mfd_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,7 @@ def build(ref: bool | None = None) -> None:
     if ref is None:
         ref = os.path.isdir("/root/reference/proj")
     if ref:
-        targets.append("ref")
+        targets += ["ref", "refapi"]   # refapi links libmagfd_b200.so: build the package first
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

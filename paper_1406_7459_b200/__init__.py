@@ -123,6 +123,10 @@ def load_library() -> C.CDLL:
         "mfd_launches_per_step": (C.c_int, [V]),
         "mfd_model_bytes_per_step": (C.c_double, [V]),
         "mfd_debug_variants": (C.c_int, [V, C.c_char_p, C.c_int]),
+        "mfd_debug_guard_check": (C.c_longlong, [V]),
+        "mfd_effective_field_f32": (C.c_int, [V, _PF, _PF, _PF]),
+        "mfd_demag_field_f32": (C.c_int, [V, _PF, _PF, _PF]),
+        "mfd_set_stepper": (C.c_int, [V, C.POINTER(_Stepper)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -301,14 +305,16 @@ class Simulation:
         self._check(self.lib.mfd_set_time(self.h, t, step))
 
     # -- field evaluation (EffectiveFieldProvider, fields.hpp:220-268)
-    def effective_field(self) -> np.ndarray:
-        out = np.zeros((3, self.n))
-        self._check(self.lib.mfd_effective_field_f64(self.h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+    def effective_field(self, dtype=np.float64) -> np.ndarray:
+        out = np.zeros((3, self.n), dtype=dtype)
+        f = self.lib.mfd_effective_field_f32 if dtype == np.float32 else self.lib.mfd_effective_field_f64
+        self._check(f(self.h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
         return out
 
-    def demag_field(self) -> np.ndarray:
-        out = np.zeros((3, self.n))
-        self._check(self.lib.mfd_demag_field_f64(self.h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+    def demag_field(self, dtype=np.float64) -> np.ndarray:
+        out = np.zeros((3, self.n), dtype=dtype)
+        f = self.lib.mfd_demag_field_f32 if dtype == np.float32 else self.lib.mfd_demag_field_f64
+        self._check(f(self.h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
         return out
 
     # -- dynamics
@@ -407,6 +413,17 @@ class Simulation:
 
     def model_bytes_per_step(self) -> float:
         return self.lib.mfd_model_bytes_per_step(self.h)
+
+    def guard_check(self) -> int:
+        """Guard-band bytes overwritten (MFD_GUARD=1 at creation; -1 when off)."""
+        return int(self.lib.mfd_debug_guard_check(self.h))
+
+    def set_stepper(self, stepper: StepperConfig):
+        """Replace the StepperConfig of the live simulation."""
+        self.stepper = stepper
+        self._s = _Stepper(stepper.dt, stepper.renormalize_every, stepper.max_steps,
+                           stepper.torque_tol_deg_per_ns, stepper.sample_every)
+        self._check(self.lib.mfd_set_stepper(self.h, C.byref(self._s)))
 
     def variants(self) -> List[str]:
         """Kernel template instantiations this context has enqueued (test hook)."""

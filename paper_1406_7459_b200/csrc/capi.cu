@@ -155,6 +155,23 @@ mfd_status mfd_effective_field_f64(mfd_ctx* c, double* x, double* y, double* z) 
 mfd_status mfd_demag_field_f64(mfd_ctx* c, double* x, double* y, double* z) {
     return guard(c, [&] { ENG(c)->field(2, x, y, z); });
 }
+mfd_status mfd_effective_field_f32(mfd_ctx* c, float* x, float* y, float* z) {
+    return guard(c, [&] { ENG(c)->field32(1, x, y, z); });
+}
+mfd_status mfd_demag_field_f32(mfd_ctx* c, float* x, float* y, float* z) {
+    return guard(c, [&] { ENG(c)->field32(2, x, y, z); });
+}
+mfd_status mfd_set_stepper(mfd_ctx* c, const mfd_stepper* s) {
+    return guard(c, [&] {
+        if (!s) throw mfd::Error(MFD_EINVAL, "mfd_set_stepper: null argument");
+        if (!(s->dt > 0)) throw mfd::Error(MFD_EINVAL, "StepperConfig: dt must be > 0");
+        if (s->renorm_every < 1) throw mfd::Error(MFD_EINVAL, "StepperConfig: renormalizeEvery must be >= 1");
+        if (!(s->torque_tol_deg_per_ns > 0))
+            throw mfd::Error(MFD_EINVAL, "StepperConfig: torque tolerance must be > 0");
+        c->st = *s;
+        ENG(c)->set_stepper(*s);
+    });
+}
 mfd_status mfd_step(mfd_ctx* c, long n, double* last, double* all) {
     return guard(c, [&] {
         if (n < 0) throw mfd::Error(MFD_EINVAL, "mfd_step: nsteps must be >= 0");
@@ -215,6 +232,11 @@ mfd_status mfd_device_state(mfd_ctx* c, void** m, long long* n, int* prec) {
     });
 }
 int mfd_launches_per_step(const mfd_ctx* c) { return c->eng->launches_per_step(); }
+long long mfd_debug_guard_check(mfd_ctx* c) {
+    long long r = -2;
+    guard(c, [&] { r = ENG(c)->guard_check(); });
+    return r;
+}
 int mfd_debug_variants(const mfd_ctx* c, char* buf, int len) {
     const std::string v = c->eng->variants();
     if (buf && len > 0) {

@@ -170,6 +170,8 @@ public:
     virtual void set_uniform(const double dir[3]) = 0;
     virtual void set_vortex(int axis) = 0;
     virtual void field(int which, double*, double*, double*) = 0;
+    virtual void field32(int which, float*, float*, float*) = 0;
+    virtual void set_stepper(const mfd_stepper& s) = 0;
     virtual void step(long n, double* last, double* all) = 0;
     virtual void step_async(long n) = 0;
     // Capture (without launching) the graphs the next step_async(n) will use;
@@ -190,6 +192,8 @@ public:
     // Kernel template instantiations enqueued since creation, one per line
     // (test hook: lets the parity tests assert which production variant ran).
     virtual std::string variants() const = 0;
+    // Test hook: guard-band bytes overwritten since creation (-1: guards off).
+    virtual long long guard_check() = 0;
     double t = 0;
     long stepno = 0;
     long long ncell = 0;
@@ -216,6 +220,8 @@ public:
     void set_uniform(const double dir[3]) override;
     void set_vortex(int axis) override;
     void field(int which, double* x, double* y, double* z) override;
+    void field32(int which, float* x, float* y, float* z) override;
+    void set_stepper(const mfd_stepper& s) override;
     void step(long n, double* last, double* all) override;
     void step_async(long n) override;
     long prepare_async(long n) override;
@@ -236,6 +242,7 @@ public:
         for (const auto& v : launched_) o += v + "\n";
         return o;
     }
+    long long guard_check() override;
 
 private:
     void note(const char* fmt, ...) {
@@ -250,6 +257,11 @@ private:
     std::set<std::string> launched_;
     void init();
     void release();
+    void* dalloc(size_t bytes);
+    struct Alloc { void* base; size_t bytes; };
+    std::vector<Alloc> allocs_;              // every persistent device buffer
+    bool guards_ = false;                    // MFD_GUARD: guard bands around each buffer
+    static constexpr size_t kGuard = 4096;
     void build_tensor(const double* host_octant);
     void enqueue(const Iter& it, int cur, bool events = false, cudaEvent_t* ev = nullptr, bool skip_k1 = false,
                  bool fwd = false);

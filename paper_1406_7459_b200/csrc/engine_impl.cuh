@@ -170,7 +170,8 @@ void Engine<T>::init() {
     lp_.wx = 1.0 / (g.dx * g.dx); lp_.wy = 1.0 / (g.dy * g.dy); lp_.wz = 1.0 / (g.dz * g.dz);
 
     const long long n = geo_.ncell;
-    auto alloc = [&](auto** p, size_t bytes) { ck(cudaMalloc((void**)p, bytes ? bytes : 16), "cudaMalloc"); };
+    guards_ = getenv("MFD_GUARD") && atoi(getenv("MFD_GUARD")) != 0;
+    auto alloc = [&](auto** p, size_t bytes) { *p = reinterpret_cast<std::remove_reference_t<decltype(*p)>>(dalloc(bytes)); };
     alloc(&M_[0], 3 * n * sizeof(T));
     alloc(&M_[1], 3 * n * sizeof(T));
     alloc(&H_, 3 * n * sizeof(T));
@@ -350,6 +351,40 @@ void Engine<T>::init() {
     ck(cudaStreamSynchronize(stream_), "setup");
 }
 
+// Device allocation of a persistent buffer.  With MFD_GUARD=1 every buffer
+// gets kGuard bytes of 0xA5 before and after it (a write-overrun detector for
+// the tests: compute-sanitizer is not available on the B200 pool);
+// guard_check() counts the guard bytes that changed.
+template <class T>
+void* Engine<T>::dalloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    const size_t pad = guards_ ? kGuard : 0;
+    void* base = nullptr;
+    ck(cudaMalloc(&base, bytes + 2 * pad), "cudaMalloc");
+    if (pad) {
+        ck(cudaMemset(base, 0xA5, pad), "guard");
+        ck(cudaMemset(static_cast<char*>(base) + pad + bytes, 0xA5, pad), "guard");
+    }
+    allocs_.push_back(Alloc{base, bytes});
+    return static_cast<char*>(base) + pad;
+}
+
+template <class T>
+long long Engine<T>::guard_check() {
+    if (!guards_) return -1;
+    ck(cudaStreamSynchronize(stream_), "sync");
+    long long bad = 0;
+    std::vector<unsigned char> h(kGuard);
+    for (const auto& a : allocs_) {
+        for (int side = 0; side < 2; ++side) {
+            const char* g = static_cast<const char*>(a.base) + (side ? kGuard + a.bytes : 0);
+            ck(cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost), "guard read");
+            for (unsigned char c : h) bad += c != 0xA5;
+        }
+    }
+    return bad;
+}
+
 template <class T>
 Engine<T>::~Engine() {
     release();
@@ -361,10 +396,8 @@ void Engine<T>::release() {
     if (stream_) cudaStreamSynchronize(stream_);
     if (cstream_) cudaStreamSynchronize(cstream_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
-    void* ptrs[] = {M_[0], M_[1], H_, A_, B_, Kt_, tw_, ybuf_, err_, torque_, sums_, partials_, ticket_, halo_};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
-    if (Ar_ && Ar_ != A_) cudaFree(Ar_);
+    for (auto& a : allocs_) cudaFree(a.base);
+    allocs_.clear();
     delete tr_;
     if (h_torque_) cudaFreeHost(h_torque_);
     if (h_sums_) cudaFreeHost(h_sums_);
@@ -1031,6 +1064,38 @@ void Engine<T>::field(int which, double* x, double* y, double* z) {
     }
 }
 
+template <class T>
+void Engine<T>::field32(int which, float* x, float* y, float* z) {
+    if (which == 2 && !terms_.demag) throw Error(MFD_ELOGIC, "lastDemagField: demag term is disabled");
+    double tq;
+    eval(which, false, tq, nullptr);
+    const long long n = geo_.ncell;
+    if constexpr (std::is_same_v<T, float>) {
+        copy3_d2h<T>(H_, x, y, z, n, stream_);
+        return;
+    }
+    ensure_stage();
+    ck(cudaMemcpyAsync(h_stage_, H_, 3 * n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaStreamSynchronize(stream_), "sync");
+    for (long long i = 0; i < n; ++i) {
+        x[i] = (float)h_stage_[i];
+        y[i] = (float)h_stage_[i + n];
+        z[i] = (float)h_stage_[i + 2 * n];
+    }
+}
+
+// Replace the stepper configuration (dt, renormalisation cadence, relax
+// limits).  dt is baked into the captured graphs' parameters: drop them.
+template <class T>
+void Engine<T>::set_stepper(const mfd_stepper& s) {
+    ck(cudaStreamSynchronize(stream_), "sync");
+    st_ = s;
+    lp_.dt = static_cast<T>(s.dt);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    graphs_.clear();
+    graph_kernels_.clear();
+}
+
 // --------------------------------------------------------------- stepping
 // Simulation<T>::step x n: renormalise iff (step+1) % renormalizeEvery == 0 (sim.hpp:38).
 template <class T>
@@ -1285,7 +1350,7 @@ void Engine<T>::timing(double ms[7]) {
     float tot = 0;
     ck(cudaEventElapsedTime(&tot, ev[0], ev[5]), "event time");
     ms[5] = tot;
-    ms[6] = 0;
+    ms[6] = tq[0];   // the step's pre-step max torque (deg/ns), as Simulation::step returns it
     for (auto& e : ev) cudaEventDestroy(e);
 }
 

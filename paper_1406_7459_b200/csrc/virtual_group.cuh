@@ -88,6 +88,21 @@ public:
         }
     }
 
+    void field32(int which, float* x, float* y, float* z) override {
+        const long long n = (long long)grid_.nx * grid_.ny * grid_.nz;
+        std::vector<double> a(n), b(n), c(n);
+        field(which, a.data(), b.data(), c.data());
+        for (long long i = 0; i < n; ++i) {
+            x[i] = (float)a[i];
+            y[i] = (float)b[i];
+            z[i] = (float)c[i];
+        }
+    }
+    void set_stepper(const mfd_stepper& s) override {
+        st_ = s;
+        for (auto& e : ranks_) e->set_stepper(s);
+    }
+
     void step(long n, double* last, double* all) override {
         for (long s = 0; s < n; ++s) {
             Iter it;
@@ -159,6 +174,15 @@ public:
     cudaStream_t stream() const override { return stream_; }
     int launches_per_step() const override { return world_ * ranks_[0]->launches_per_step(); }
     double model_bytes() const override { return world_ * ranks_[0]->model_bytes(); }
+    long long guard_check() override {
+        long long s = 0;
+        for (auto& e : ranks_) {
+            const long long b = e->guard_check();
+            if (b < 0) return -1;
+            s += b;
+        }
+        return s;
+    }
     std::string variants() const override {
         std::set<std::string> all;
         for (const auto& e : ranks_) {

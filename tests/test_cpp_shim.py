@@ -65,3 +65,56 @@ def test_formats_shim_driver(tmp_path):
     assert "ConfigError config line 1: grid.nx must be >= 1, got 0" in out
     assert "IoError cannot open for reading: " in out
     assert (tmp_path / "t.csv").read_text().splitlines()[1] == "0,0,1,0,0,1,2,3,4,10,0.5"
+
+
+# ---- drop-in form: the same driver body against magfd::Simulation<T> and magfd_b200::Simulation<T>
+REFAPI = os.path.join(ROOT, "oracle", "_ref", "refapi_driver")
+
+
+def test_refapi_driver_builds_against_reference_headers():
+    """tests/cpp/refapi_driver.cpp instantiates one reference-style driver body with the
+    reference's Simulation<T>(SimSpec, Backend) and with magfd_b200::Simulation<T>; it
+    compiles only if the shim's signatures and result types are the reference's."""
+    if not os.path.isdir("/root/reference/proj"):
+        pytest.skip("reference sources absent (prebuilt oracle/_ref/refapi_driver is used on the GPU box)")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "refapi"], check=True)
+    assert os.path.exists(REFAPI)
+    out = subprocess.run([REFAPI, "64", "ref", "/tmp"], check=True, capture_output=True, text=True).stdout
+    assert out.startswith("torque 0 ") and "relax " in out
+
+
+def _parse(out):
+    d = {"torque": [], "sample": []}
+    for l in out.splitlines():
+        k, *v = l.split()
+        if k in ("torque", "sample"):
+            d[k].append([float(x) for x in v])
+        else:
+            d[k] = v
+    return d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [64, 32])
+def test_refapi_driver_b200_matches_reference(prec, tmp_path):
+    if not os.path.exists(REFAPI):
+        pytest.skip("oracle/_ref/refapi_driver not built")
+    ref = _parse(subprocess.run([REFAPI, str(prec), "ref", str(tmp_path)], check=True, capture_output=True,
+                                text=True).stdout)
+    mine = _parse(subprocess.run([REFAPI, str(prec), "b200", str(tmp_path)], check=True, capture_output=True,
+                                 text=True).stdout)
+    tol = 1e-9 if prec == 64 else 2e-5
+    t_ref, t_mine = np.array(ref["torque"]), np.array(mine["torque"])
+    assert np.array_equal(t_ref[:, 0], t_mine[:, 0])
+    assert np.max(np.abs(t_mine[:, 1] - t_ref[:, 1]) / t_ref[:, 1]) <= tol
+    s_ref, s_mine = np.array(ref["sample"]), np.array(mine["sample"])
+    assert np.array_equal(s_ref[:, :2], s_mine[:, :2])                     # step, t
+    assert np.max(np.abs(s_mine[:, 2:5] - s_ref[:, 2:5])) <= 10 * tol       # <m>
+    assert np.max(np.abs(s_mine[:, 5] - s_ref[:, 5]) / np.abs(s_ref[:, 5])) <= 10 * tol
+    assert mine["timing_positive"] == ["1"]
+    msum_r, msum_m = np.array(ref["msum"], float), np.array(mine["msum"], float)
+    assert np.max(np.abs(msum_m - msum_r)) <= tol * np.max(np.abs(msum_r)) * 10
+    assert mine["relax"][:4] == ref["relax"][:4]                             # converged, samples, steps
+    csv_ref = (tmp_path / "ref.csv").read_text().splitlines()
+    csv_mine = (tmp_path / "b200.csv").read_text().splitlines()
+    assert csv_ref[0] == csv_mine[0] and len(csv_ref) == len(csv_mine)      # written by io::writeTrajectoryCsv
