@@ -193,14 +193,5 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
-// Explicit fused multiply-add / reciprocal square root for the production K5
-// epilogue (demag on: the bar is 1e-5 / 1e-10 relative, not bitwise).  Written
-// as intrinsics, not left to contraction, so every K5 instantiation rounds
-// identically (the fused / unfused / sampling / multi-rank variants must stay
-// bitwise equal to each other).
-__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
-__device__ __forceinline__ float rsqrt_(float a) { return rsqrtf(a); }
-__device__ __forceinline__ double rsqrt_(double a) { return rsqrt(a); }
 
 } // namespace mfd

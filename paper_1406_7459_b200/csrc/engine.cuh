@@ -49,10 +49,6 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr double kMu0 = 4.0e-7 * kPi;                       // constants.hpp:9
 constexpr double kRadToDegPerNs = 180.0 / kPi * 1e-9;       // dynamics.hpp:34
 constexpr int kMaxL = 2048;
-// Pipelined persistent K1 (cp.async staging).  Measured on B200 at
-// 512x512x64 f32 it is not faster than the plain K1 (0.33 vs 0.27 ms at 232
-// registers); kept selectable for further tuning.
-constexpr bool kUseK1Pipe = false;
 // Fuse the next step's x pass (K1) into K5 inside a graph chunk.
 constexpr bool kFuseK1 = true;
 // One-kernel K2-K4 for thin / small grids (YZCfg::OK).
@@ -329,9 +325,7 @@ private:
     int* h_perr_ = nullptr;                    // pinned [kMaxPending]
     T* h_stage_ = nullptr;                     // pinned 3N staging
     long long k5_blocks_ = 1;
-    bool k1_pipe_ = false;                     // pipelined persistent K1 usable for this grid
     bool small_x_ = false;                     // few rows: small-CTA variants of K1 / K5
-    int k1_grid_ = 1, k1_smem_ = 0;
     int stop_after_ = 0;                       // debug_stage: stop the pipeline after K<n>
     bool fuse_k1_ = false;                     // K5 also runs the next step's K1 (within a graph chunk)
     bool yz_small_ = false;                    // K2-K4 as one kernel (k_fft_yz_small)

@@ -221,20 +221,6 @@ void Engine<T>::init() {
         with_pow2(geo_.N, [&]<int L>() {
             set_smem<T>((const void*)k_r2c_x<T, L>, XCfg<T, L>::SMEM);
             if (G > 1) set_smem<T>((const void*)k_r2c_x<T, L, 0, true>, XCfg<T, L>::SMEM);
-            // pipelined K1: persistent grid sized by occupancy
-            k1_pipe_ = kUseK1Pipe && G == 1 && L >= 2 && g.nx % 2 == 0 && (geo_.ncell * (long long)sizeof(T)) % 16 == 0;
-            if constexpr (L >= 2) if (k1_pipe_) {
-                const int sm_bytes = XCfg<T, L>::SMEM + 2 * XCfg<T, L>::ROWS * L * (int)sizeof(T);
-                set_smem<T>((const void*)k_r2c_x_pipe<T, L>, sm_bytes);
-                int per_sm = 0, nsm = 0;
-                ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r2c_x_pipe<T, L>, XCfg<T, L>::NT,
-                                                                 sm_bytes),
-                   "occupancy");
-                ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_), "attr");
-                const long long tiles = 3 * ((nrows + XCfg<T, L>::ROWS - 1) / XCfg<T, L>::ROWS);
-                k1_grid_ = (int)std::min<long long>(tiles, (long long)std::max(1, per_sm) * nsm);
-                k1_smem_ = sm_bytes;
-            }
             set_smem<T>((const void*)k_c2r_x_llg<T, L>, LCfg<T, L>::SMEM, false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, true>, k5_smem<T, L, 0, false>(), false);
             set_smem<T>((const void*)k_c2r_x_llg_v<T, L, false>, k5_smem<T, L, 0, false>(), false);
@@ -592,12 +578,7 @@ void Engine<T>::enq_A(const Iter& it, int cur, cudaEvent_t* ev, bool skip_k1) {
     const long long nrows = (long long)geo_.ny * geo_.nz;
     if (!skip_k1) with_pow2(geo_.N, [&]<int L>() {
         using CF = XCfg<T, L>;
-        if (k1_pipe_) {
-            if constexpr (L >= 2) {
-                note("K1 k_r2c_x_pipe<%s,%d>", tn(), L);
-                k_r2c_x_pipe<T, L><<<k1_grid_, CF::NT, k1_smem_, stream_>>>(geo_, M_[cur], A_, tw_, ctl);
-            }
-        } else if (small_x_) {
+        if (small_x_) {
             if constexpr (L >= 2 && L <= kSmallXMax) {
                 using CS = XCfg<T, L, 2>;
                 dim3 grid((unsigned)((nrows + 1) / 2), 3);

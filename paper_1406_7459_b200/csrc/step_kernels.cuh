@@ -38,9 +38,6 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
     static constexpr int NT = RS > 0 ? clampNT(ROWS * N / E) : clampNT(cmax(128, ROWS * N / E));
     static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
 };
-#ifndef MFD_K5_STAGE
-#define MFD_K5_STAGE 0   // measured slower at C4 (2 CTAs/SM): 0.372 -> 0.455 ms
-#endif
 #ifndef MFD_Y_TILE_MAX
 // bytes of the K2/K4 shared tile (W columns x L).  64 KB keeps 2+ CTAs/SM;
 // the three-stage Py = 2048 pass (C5) is faster with 128 KB tiles, i.e.
@@ -49,18 +46,6 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #endif
 #ifndef MFD_Z2_W
 #define MFD_Z2_W 0             // K3 (two-stage) columns per CTA override (0: default)
-#endif
-#ifndef MFD_K3_KPF
-#define MFD_K3_KPF 0           // K3: L2 prefetch of the CTA's tensor bins at kernel entry
-#endif
-#ifndef MFD_NO_HALT
-#define MFD_NO_HALT 0          // measurement only: drop the per-CTA halt check
-#endif
-#ifndef MFD_K3_ASYNC
-#define MFD_K3_ASYNC 1         // K3 stage-0 inputs of all three components in flight at once (cp.async)
-#endif
-#ifndef MFD_K5_STG_MINB
-#define MFD_K5_STG_MINB 0      // resident CTAs/SM the staged K5's register budget assumes (0: as unstaged)
 #endif
 #ifndef MFD_YFWD_F64_MINB
 #define MFD_YFWD_F64_MINB 2   // f64 K2 (non-TMA y forward): 128 registers, 2 CTAs/SM (C4 f64 K2 0.713 -> 0.631 ms)
@@ -71,30 +56,15 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K5_F64_MINB
 #define MFD_K5_F64_MINB 2   // f64 K5: 128 registers, 2 CTAs/SM (C4 f64 K5 1.196 -> 0.949 ms despite a 144-byte spill)
 #endif
-#ifndef MFD_K5_STAGE_MAX
-#define MFD_K5_STAGE_MAX 113   // KB of shared memory per CTA the staged K5 may use
-#endif
 template <class T, int N, int RS = 0> struct LCfg {   // K5
     static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(32, 2048 / cmax(N, 1)));
     static constexpr int NT = RS > 0 ? 64 : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
-    // STG: the CTA's M rows and their two in-plane y-neighbour rows are
-    // staged into shared memory by cp.async at kernel start, so their L2
-    // latency overlaps the inverse x FFT; the epilogue then reads M, its x
-    // and y neighbours from shared memory and only the z rows from L2.
-    static constexpr int SROWS = ROWS + 2;
-    static constexpr int SOFF = (SMEM + 15) / 16 * 16;   // 16-byte aligned staging offset
-    static constexpr bool STG = MFD_K5_STAGE && sizeof(T) == 4 && RS == 0 && ROWS >= 4 &&
-                                SOFF + 3 * SROWS * N * (int)sizeof(T) <= MFD_K5_STAGE_MAX * 1024;
-    static constexpr int MINB = sizeof(T) == 4 ? (STG && MFD_K5_STG_MINB > 0 ? MFD_K5_STG_MINB
-                                                                         : cmax(1, cmin(3, (200 * 1024) / SMEM)))
+    static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
                                                : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
-    static constexpr int SMEM_STG = STG ? SOFF + 3 * SROWS * N * (int)sizeof(T) : SMEM;
 };
-// dynamic shared memory of a K5 variant (the fused-K1 variant does not stage M)
-template <class T, int N, int RS, bool FWD> constexpr int k5_smem() {
-    return FWD ? LCfg<T, N, RS>::SMEM : LCfg<T, N, RS>::SMEM_STG;
-}
+// dynamic shared memory of a K5 variant
+template <class T, int N, int RS, bool FWD> constexpr int k5_smem() { return LCfg<T, N, RS>::SMEM; }
 template <class T, int L> struct YCfg {   // K2 / K4
     static constexpr int CS = sizeof(C2<T>);
     static constexpr int W = cmax(1, cmin(128 / CS, MFD_Y_TILE_MAX(L) / (L * CS)));   // <= 64 KB tile: 2+ CTAs/SM
@@ -183,27 +153,16 @@ template <class T> struct Halo { const T* lo; const T* hi; };
 
 // Step control: early exit after a non-finite update (error) or, in relax
 // mode, once the previous iteration met the torque criterion
-// (dynamics.hpp:180-188).
+// (dynamics.hpp:180-188).  Only K1 and K5 check it: the y / z passes (K2-K4)
+// read and write nothing but the A / B spectrum scratch, so running them on a
+// halted iteration is harmless, and skipping the dependent flag load at the
+// entry of every K2-K4 CTA saves ~1 % of the step (C4 f32: K3 0.555 -> 0.541 ms).
 struct Ctl {
     int* err;                                   // 0 ok, else failing iteration + 1
     const unsigned long long* prev_torque;      // null: no convergence check
     double Ms, tol, rad2deg;
 };
-// The y / z passes (K2-K4) only read and write the A / B spectrum scratch, so
-// running them on a halted iteration is harmless: K5 (which writes M, the
-// torque and the sums) and K1 keep the check.  Skipping the dependent flag load
-// at the entry of every K2-K4 CTA saves ~1 % of the step (C4 f32: K3 0.555 ->
-// 0.541 ms).
-#ifndef MFD_MID_HALT
-#define MFD_MID_HALT 0
-#endif
-__device__ __forceinline__ bool halted(const Ctl& c);
-__device__ __forceinline__ bool halted_mid(const Ctl& c) {
-    if constexpr (MFD_MID_HALT) return halted(c);
-    else return false;
-}
 __device__ __forceinline__ bool halted(const Ctl& c) {
-    if (MFD_NO_HALT) return false;
     if (*(volatile int*)c.err) return true;
     if (c.prev_torque) {
         const double r = __longlong_as_double((long long)*(volatile unsigned long long*)c.prev_torque);
@@ -341,77 +300,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int K>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory"); }
 
-// K1, pipelined persistent form: each CTA walks (component, row group)
-// tiles; the ROWS consecutive M rows of the NEXT tile (one contiguous span)
-// stream into a shared staging buffer with cp.async while the current tile
-// is transformed, so HBM latency overlaps the FFT instead of stalling it.
-// Needs nx even and 16-byte aligned component planes (checked on the host).
-template <class T, int N>
-__global__ void __launch_bounds__(XCfg<T, N>::NT, 3)
-k_r2c_x_pipe(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
-    using CF = XCfg<T, N>;
-    constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>();
-    constexpr int VEC = 16 / sizeof(T);
-    if (halted(ctl)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
-    T* stage[2] = {reinterpret_cast<T*>(sm + ROWS * LP), reinterpret_cast<T*>(sm + ROWS * LP) + ROWS * N};
-    const long long nrows = (long long)g.ny * g.nz;
-    const int ngroups = (int)((nrows + ROWS - 1) / ROWS);
-    const int ntiles = 3 * ngroups;
-    const int nx = g.nx;
-    auto fetch = [&](int t, T* buf) {
-        const int comp = t / ngroups, grp = t % ngroups;
-        const long long r0 = (long long)grp * ROWS;
-        const long long rows = nrows - r0 < ROWS ? nrows - r0 : ROWS;
-        const T* src = M + comp * g.ncell + r0 * nx;
-        const int chunks = (int)(rows * nx / VEC);
-        for (int q = threadIdx.x; q < chunks; q += NT) cp_async16(buf + q * VEC, src + q * VEC);
-    };
-    int t = blockIdx.x;
-    if (t < ntiles) fetch(t, stage[0]);
-    cp_commit();
-    for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
-        if (t + (int)gridDim.x < ntiles) fetch(t + gridDim.x, stage[(it + 1) & 1]);
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
-        const T* in = stage[it & 1];
-        const int comp = t / ngroups;
-        const long long row0 = (long long)(t % ngroups) * ROWS;
-        auto ld0 = [&](int col, int pos) -> C2<T> {
-            const int i0 = 2 * pos;
-            if (row0 + col >= nrows || i0 >= nx) return mk<T>(0, 0);
-            return *reinterpret_cast<const C2<T>*>(in + col * nx + i0);
-        };
-        auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
-        auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
-        fft_forward<T, N, ROWS, NT, false, false, true, true, true>(ld0, lds, sts, sts, tw);
-        __syncthreads();
-        auto post = [&](int col, int k) {
-            const C2<T> zk = sm[col * LP + xpad<T>(k & (N - 1))];
-            const C2<T> zn = cconj<T>(sm[col * LP + xpad<T>((N - k) & (N - 1))]);
-            const C2<T> E = cscale<T>(cadd<T>(zk, zn), T(0.5));
-            const C2<T> d = csub<T>(zk, zn);
-            const C2<T> O = mk<T>(T(0.5) * d.y, T(-0.5) * d.x);
-            const C2<T> w = __ldg(tw_dense<T, 2 * N>(tw) + k);
-            const C2<T> wo = cmul<T>(w, O);
-            C2<T>* dst = A + ((long long)comp * nrows + row0 + col) * g.Hp;
-            dst[k] = cadd<T>(E, wo);
-            if (N - k != k) dst[N - k] = cconj<T>(csub<T>(E, wo));
-        };
-        constexpr int HP = N / 2;
-        for (int e = threadIdx.x; e < ROWS * HP; e += NT) {
-            const int col = e / HP, k = e % HP;
-            if (row0 + col >= nrows) continue;
-            post(col, k);
-            if (k == 0) post(col, N / 2);
-        }
-        __syncthreads();   // staging buffer and work tile are reused next iteration
-    }
-    cp_wait<0>();
-}
-
 // ------------------------------------------------------------------ K2
 // Tiles of W x-bins never leave the padded pitch (Hp and Wb are multiples of
 // 16 >= W), so x-bins >= Hx are computed as harmless padding columns instead
@@ -423,7 +311,7 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
             int comp0) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
@@ -463,7 +351,7 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     using CF = YTCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
     constexpr int TWL = kK2StridedTw ? TWN : L;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* work = reinterpret_cast<C2<T>*>(smem_raw);
     // TMA destinations must be 128-byte aligned
@@ -521,7 +409,7 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
             int comp0) {
     using CF = YCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;
@@ -570,7 +458,7 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
                 const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int comp0, int ncomp) {
     using CF = YICfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT, R0 = CF::R0, R1 = CF::R1, HALF = CF::HALF;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* slot0 = align128(reinterpret_cast<C2<T>*>(smem_raw));
     __shared__ uint64_t bar[3];
@@ -670,7 +558,7 @@ k_fft_z_conv(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T>
              const int* __restrict__ ybuf, Ctl ctl) {
     using CF = ZCfg<T, L>;
     constexpr int W = CF::W, NCOL = CF::NCOL, NT = CF::NT;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;               // x-bin within this rank's block
@@ -805,7 +693,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     constexpr int W = CF::W, NCOL = CF::NCOL, R0 = CF::R0, R1 = CF::R1;
     constexpr int CO = CF::NROW * W;   // column stride of the components
     static_assert(Plan<T, L>::S == 2 && R0 % R1 == 0, "two-stage plans with R0 % R1 == 0 only");
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const int u0 = blockIdx.x * W;               // x-bin within this rank's block
@@ -821,18 +709,15 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + k*S_k
     // smem column of (comp c, row r, bin w): c*CO + r*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + (SROW ? 0 : r * W) + w;
-    if constexpr (MFD_K3_KPF) {   // tensor bins (v, all w, this CTA's W bins) -> L2
-        const int Hz2 = L / 2 + 1;
-        for (int wq = threadIdx.x; wq < Hz2; wq += CF::NT)
-            l2_prefetch(Kt + (((long long)v * Hz2 + wq) * Wb + u0) * 6, (long long)W * 6 * sizeof(T));
-    }
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
-    if constexpr (MFD_K3_ASYNC) {
+    {
         // All three components' inputs go into flight at kernel entry as
         // cp.async copies into the thread's own shared-memory slots (the
         // positions R1*j + n2 its stage-0 task reads and then overwrites), one
         // commit group per component: no staging registers, and the HBM
-        // latency of components 1 and 2 hides behind component 0's DFT.
+        // latency of components 1 and 2 hides behind component 0's DFT
+        // (C4 f32: 0.584 -> 0.553 ms against a register pipeline that fetched
+        // component c+1 while transforming c).
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
 #pragma unroll
@@ -861,35 +746,6 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
 #pragma unroll
             for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * CO] = x[k];
         }
-    } else {
-    // Software pipeline over the three components: the loads of component
-    // c+1 are in flight while component c is transformed.  (A persistent
-    // variant that also prefetched the next tile measured slower on B200:
-    // 0.88 vs 0.69 ms at 512x512x64 f32, the tensor loads lost their overlap.)
-    C2<T> nxt[R0 / 2];
-    auto fetch = [&](int c) {
-#pragma unroll
-        for (int j = 0; j < R0 / 2; ++j) {
-            const int pos = R1 * j + n2;
-            nxt[j] = (live && (FZ || pos < nz)) ? gcol[c * cstride + (long long)pos * g.S_k] : mk<T>(0, 0);
-        }
-    };
-    fetch(0);
-    C2<T> twr[R0];
-#pragma unroll
-    for (int k = 1; k < R0; ++k) twr[k] = __ldg(tw_dense<T, L>(tw) + n2 * k);
-#pragma unroll 1
-    for (int c = 0; c < 3; ++c) {
-        C2<T> x[R0];
-#pragma unroll
-        for (int j = 0; j < R0; ++j) x[j] = 2 * j < R0 ? nxt[j] : mk<T>(0, 0);
-        if (c < 2) fetch(c + 1);
-        dft<T, R0, false, true>(x);
-#pragma unroll
-        for (int k = 1; k < R0; ++k) x[k] = cmul<T>(x[k], twr[k]);
-#pragma unroll
-        for (int k = 0; k < R0; ++k) scol[(k * R1 + n2) * NCOL + c * CO] = x[k];
-    }
     }
     // ---- stage 1 + tensor product + inverse stage 1, in registers.  The
     // tensor bins of iteration it are loaded one phase ahead (before the
@@ -975,7 +831,7 @@ constexpr int z_variant() {
 template <class T, int L>
 __global__ void __launch_bounds__(64)
 k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int* __restrict__ ybuf, Ctl ctl) {
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     const int w = threadIdx.x & 31, r = threadIdx.x >> 5;
     const int u = blockIdx.x * 32 + w;           // x-bin within this rank's block
     const int v = blockIdx.y;
@@ -1035,7 +891,7 @@ k_fft_yz_small(Geo g, C2<T>* __restrict__ A, const T* __restrict__ Kt, const C2<
                const int* __restrict__ ybuf, Ctl ctl) {
     using CF = YZCfg<T, LY, LZ>;
     constexpr int W = CF::W, NZH = CF::NZH, NCOL = CF::NCOL, NT = CF::NT;
-    if (halted_mid(ctl)) return;
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);    // [y position][NCOL]
     const int u0 = blockIdx.x * W;
@@ -1344,102 +1200,6 @@ k_c2r_x_llg(Geo g, const C2<T>* __restrict__ A, const T* __restrict__ M, T* __re
     block_finish<NT>(io, ctl, tmax, acc, bad);
 }
 
-// Per-cell H_eff + LLG + Euler from register values, reference operation
-// order (identical arithmetic to cell_update).  nb: neighbours x-, x+, y-,
-// y+, z-, z+ (only read where has[] is set, Neumann boundaries).
-template <class T>
-__device__ __forceinline__ void cell_core(const LocalParams<T>& P, const StepIO& io, T mx, T my, T mz,
-                                          const T (&nb)[6][3], const bool (&has)[6], T hdx, T hdy, T hdz,
-                                          T (&mo)[3], T (&ho)[3], double& tmax, double* acc, int& bad,
-                                          bool& write) {
-    T Hx = hdx, Hy = hdy, Hz = hdz;
-    double elink = 0;
-    if (P.exch) {
-        T h0 = 0, h1 = 0, h2 = 0;
-        const T wv[6] = {P.cx, P.cx, P.cy, P.cy, P.cz, P.cz};
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            if (has[q]) {
-                h0 = add_rn(h0, mul_rn(wv[q], sub_rn(nb[q][0], mx)));
-                h1 = add_rn(h1, mul_rn(wv[q], sub_rn(nb[q][1], my)));
-                h2 = add_rn(h2, mul_rn(wv[q], sub_rn(nb[q][2], mz)));
-            }
-        }
-        if (io.sums) {
-            const double ww[3] = {P.wx, P.wy, P.wz};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                if (has[2 * a + 1]) {
-                    const double e0 = (double)nb[2 * a + 1][0] - mx, e1 = (double)nb[2 * a + 1][1] - my,
-                                 e2 = (double)nb[2 * a + 1][2] - mz;
-                    elink += ww[a] * (e0 * e0 + e1 * e1 + e2 * e2);
-                }
-            }
-        }
-        Hx = add_rn(Hx, h0);
-        Hy = add_rn(Hy, h1);
-        Hz = add_rn(Hz, h2);
-    }
-    if (P.anis) {
-        const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
-        Hx = add_rn(Hx, mul_rn(proj, P.ax));
-        Hy = add_rn(Hy, mul_rn(proj, P.ay));
-        Hz = add_rn(Hz, mul_rn(proj, P.az));
-    }
-    if (P.zee) {
-        Hx = add_rn(Hx, P.hx);
-        Hy = add_rn(Hy, P.hy);
-        Hz = add_rn(Hz, P.hz);
-    }
-    if (io.write_h == 1) {
-        ho[0] = Hx; ho[1] = Hy; ho[2] = Hz;
-    } else {
-        ho[0] = hdx; ho[1] = hdy; ho[2] = hdz;
-    }
-    if (io.sums) {
-        acc[0] += (double)mx;
-        acc[1] += (double)my;
-        acc[2] += (double)mz;
-        acc[3] += elink;
-        const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
-        const double p = m0 * P.dax + m1 * P.day + m2 * P.daz;
-        acc[4] += 1.0 - p * p;
-        acc[5] += (double)hdx * mx + (double)hdy * my + (double)hdz * mz;
-        acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
-    }
-    const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
-    const T c0 = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
-    const T c1 = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
-    const T c2 = sub_rn(mul_rn(mx, b1), mul_rn(my, b0));
-    const T d0 = sub_rn(mul_rn(my, c2), mul_rn(mz, c1));
-    const T d1 = sub_rn(mul_rn(mz, c0), mul_rn(mx, c2));
-    const T d2 = sub_rn(mul_rn(mx, c1), mul_rn(my, c0));
-    const T r0 = add_rn(mul_rn(P.precess, c0), mul_rn(P.damp, d0));
-    const T r1 = add_rn(mul_rn(P.precess, c1), mul_rn(P.damp, d1));
-    const T r2 = add_rn(mul_rn(P.precess, c2), mul_rn(P.damp, d2));
-    {
-        const double v0 = r0, v1 = r1, v2 = r2;
-        tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
-    }
-    write = false;
-    if (io.update) {
-        T e0 = add_rn(mx, mul_rn(P.dt, r0));
-        T e1 = add_rn(my, mul_rn(P.dt, r1));
-        T e2 = add_rn(mz, mul_rn(P.dt, r2));
-        if (io.renorm) {
-            const T n2 = add_rn(add_rn(mul_rn(e0, e0), mul_rn(e1, e1)), mul_rn(e2, e2));
-            if (!(n2 > T(0)) || !isfinite((double)n2)) { bad = 1; return; }
-            const T f = P.Ms / sqrt(n2);
-            e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
-        } else if (!isfinite((double)add_rn(add_rn(e0, e1), e2))) {
-            bad = 1;
-            return;
-        }
-        mo[0] = e0; mo[1] = e1; mo[2] = e2;
-        write = true;
-    }
-}
-
 // 16-byte vector of V = 16/sizeof(T) consecutive cells.
 template <class T> struct V16;
 template <> struct V16<float> { using type = float4; static constexpr int V = 4; };
@@ -1473,28 +1233,16 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // The exchange field of component c needs only component c of the
 // neighbours, so the stencil runs one component at a time (register use
 // independent of the component count); per cell and component the sum is
-// accumulated in the reference order x-, x+, y-, y+, z-, z+ (fields.hpp:33-48).
-// fsm (fused next-step x pass): the new M of the V cells also goes to shared
-// memory as (x[2n], x[2n+1]) pairs at component stride fstride.
-// STG: ms = the staged copy of this row (component 0, x = 0) in shared
-// memory, component stride mcs, row pitch mpitch (rows j-1 and j+1 of the
-// same plane are the adjacent staged rows).
-// FAST: fused multiply-adds and an approximate reciprocal square root for the
-// renormalisation (the production K5; the bitwise
-// reference-order form stays in cell_update / k_local_llg and FAST = false).
-#ifndef MFD_K5_FAST
-#define MFD_K5_FAST 0   // measured at C4 f32: FMA epilogue 0.384 vs 0.377 ms (strict), kept for A/B
-#endif
-#ifndef MFD_K5_ASYNC
-#define MFD_K5_ASYNC 0   // cp.async-staged spectrum rows: 0.395 vs 0.384 ms at C4 f32 (register loads win)
-#endif
-template <class T, bool SUMS, bool STG = false, bool FAST = MFD_K5_FAST>
+// accumulated in the reference order x-, x+, y-, y+, z-, z+ (fields.hpp:33-48),
+// with separate round-to-nearest multiplies and adds as the reference build
+// (no FMA).  fsm (fused next-step x pass): the new M of the V cells also goes
+// to shared memory as (x[2n], x[2n+1]) pairs at component stride fstride.
+template <class T, bool SUMS>
 __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
                                           const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
                                           const Halo<T>& hl, long long c0, int i0, int j, int k,
                                           const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
-                                          C2<T>* fsm = nullptr, int fstride = 0,
-                                          const T* ms = nullptr, int mcs = 0, int mpitch = 0) {
+                                          C2<T>* fsm = nullptr, int fstride = 0) {
     constexpr int V = V16<T>::V;
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
     const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
@@ -1508,8 +1256,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const T* p = M + c * n + c0;
-        const T* sp = STG ? ms + c * mcs + i0 : nullptr;
-        if (STG) vlds<T>(sp, m[c]); else vload<T>(p, m[c]);
+        vload<T>(p, m[c]);
         if (!P.exch) {
 #pragma unroll
             for (int q = 0; q < V; ++q) H[c][q] = hd[c][q];
@@ -1518,30 +1265,21 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         T ym[V], yp[V], zm[V], zp[V];
         if (hz0) vload<T>(k > 0 ? p - sz : hl.lo + c * sz + inplane, zm);          // slab edge: halo plane
         if (hz1) vload<T>(k < g.nz - 1 ? p + sz : hl.hi + c * sz + inplane, zp);
-        if (STG) {
-            if (hy0) vlds<T>(sp - mpitch, ym);
-            if (hy1) vlds<T>(sp + mpitch, yp);
-        } else {
-            if (hy0) vload<T>(p - sy, ym);
-            if (hy1) vload<T>(p + sy, yp);
-        }
-        const T xl = hx0 ? (STG ? sp[-1] : __ldg(p - 1)) : T(0);
-        const T xr = hx1 ? (STG ? sp[V] : __ldg(p + V)) : T(0);
+        if (hy0) vload<T>(p - sy, ym);
+        if (hy1) vload<T>(p + sy, yp);
+        const T xl = hx0 ? __ldg(p - 1) : T(0);
+        const T xr = hx1 ? __ldg(p + V) : T(0);
 #pragma unroll
         for (int q = 0; q < V; ++q) {
             const T mc = m[c][q];
             const T xm = q > 0 ? m[c][q - 1] : xl, xp = q < V - 1 ? m[c][q + 1] : xr;
             T h = 0;
-            auto ex = [&](T w, T nb) {   // fields.hpp:33-48: h += w (M_nbr - M_c)
-                if constexpr (FAST) h = fma_rn(w, sub_rn(nb, mc), h);
-                else h = add_rn(h, mul_rn(w, sub_rn(nb, mc)));
-            };
-            if (q > 0 || hx0) ex(P.cx, xm);
-            if (q < V - 1 || hx1) ex(P.cx, xp);
-            if (hy0) ex(P.cy, ym[q]);
-            if (hy1) ex(P.cy, yp[q]);
-            if (hz0) ex(P.cz, zm[q]);
-            if (hz1) ex(P.cz, zp[q]);
+            if (q > 0 || hx0) h = add_rn(h, mul_rn(P.cx, sub_rn(xm, mc)));
+            if (q < V - 1 || hx1) h = add_rn(h, mul_rn(P.cx, sub_rn(xp, mc)));
+            if (hy0) h = add_rn(h, mul_rn(P.cy, sub_rn(ym[q], mc)));
+            if (hy1) h = add_rn(h, mul_rn(P.cy, sub_rn(yp[q], mc)));
+            if (hz0) h = add_rn(h, mul_rn(P.cz, sub_rn(zm[q], mc)));
+            if (hz1) h = add_rn(h, mul_rn(P.cz, sub_rn(zp[q], mc)));
             H[c][q] = add_rn(hd[c][q], h);
             if (SUMS) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
                 if (q < V - 1 || hx1) { const double e = (double)xp - mc; elink[q] += P.wx * e * e; }
@@ -1556,63 +1294,6 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
     for (int q = 0; q < V; ++q) {
         const T mx = m[0][q], my = m[1][q], mz = m[2][q];
         T Hx = H[0][q], Hy = H[1][q], Hz = H[2][q];
-        if constexpr (FAST) {
-            if (P.anis) {
-                const T proj = mul_rn(P.ca, fma_rn(mx, P.ax, fma_rn(my, P.ay, mul_rn(mz, P.az))));
-                Hx = fma_rn(proj, P.ax, Hx);
-                Hy = fma_rn(proj, P.ay, Hy);
-                Hz = fma_rn(proj, P.az, Hz);
-            }
-            if (P.zee) {
-                Hx = add_rn(Hx, P.hx);
-                Hy = add_rn(Hy, P.hy);
-                Hz = add_rn(Hz, P.hz);
-            }
-            if (io.write_h == 1) { H[0][q] = Hx; H[1][q] = Hy; H[2][q] = Hz; }
-            if (SUMS) {
-                acc[0] += (double)mx;
-                acc[1] += (double)my;
-                acc[2] += (double)mz;
-                acc[3] += elink[q];
-                const double m0 = (double)mx / P.dMs, m1 = (double)my / P.dMs, m2 = (double)mz / P.dMs;
-                const double pp = m0 * P.dax + m1 * P.day + m2 * P.daz;
-                acc[4] += 1.0 - pp * pp;
-                acc[5] += (double)hd[0][q] * mx + (double)hd[1][q] * my + (double)hd[2][q] * mz;
-                acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
-            }
-            // llgRhs (dynamics.hpp:49-64): b = mu0 H, c = m x b, d = m x c, r = P c + D d
-            const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
-            const T c0x = fma_rn(my, b2, -mul_rn(mz, b1));
-            const T c1x = fma_rn(mz, b0, -mul_rn(mx, b2));
-            const T c2x = fma_rn(mx, b1, -mul_rn(my, b0));
-            const T d0 = fma_rn(my, c2x, -mul_rn(mz, c1x));
-            const T d1 = fma_rn(mz, c0x, -mul_rn(mx, c2x));
-            const T d2 = fma_rn(mx, c1x, -mul_rn(my, c0x));
-            const T r0 = fma_rn(P.precess, c0x, mul_rn(P.damp, d0));
-            const T r1 = fma_rn(P.precess, c1x, mul_rn(P.damp, d1));
-            const T r2 = fma_rn(P.precess, c2x, mul_rn(P.damp, d2));
-            {   // maxTorqueRate in double (dynamics.hpp:75-82): |rhs|^2 overflows float
-                const double v0 = r0, v1 = r1, v2 = r2;
-                tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
-            }
-            // eulerUpdate (dynamics.hpp:93-121)
-            T e0 = fma_rn(P.dt, r0, mx);
-            T e1 = fma_rn(P.dt, r1, my);
-            T e2 = fma_rn(P.dt, r2, mz);
-            if (io.renorm) {
-                const T n2 = fma_rn(e0, e0, fma_rn(e1, e1, mul_rn(e2, e2)));
-                if (!(n2 > T(0)) || !isfinite(n2)) {
-                    all = false;
-                } else {
-                    const T f = mul_rn(P.Ms, rsqrt_(n2));
-                    e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
-                }
-            } else if (!isfinite(add_rn(add_rn(e0, e1), e2))) {
-                all = false;
-            }
-            mo[0][q] = e0; mo[1][q] = e1; mo[2][q] = e2;
-            continue;
-        }
         if (P.anis) {
             const T proj = mul_rn(P.ca, add_rn(add_rn(mul_rn(mx, P.ax), mul_rn(my, P.ay)), mul_rn(mz, P.az)));
             Hx = add_rn(Hx, mul_rn(proj, P.ax));
@@ -1636,6 +1317,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             acc[5] += (double)hd[0][q] * mx + (double)hd[1][q] * my + (double)hd[2][q] * mz;
             acc[6] += P.dhx * mx + P.dhy * my + P.dhz * mz;
         }
+        // llgRhs (dynamics.hpp:49-64): b = mu0 H, c = m x b, d = m x c, r = P c + D d
         const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
         const T c0x = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
         const T c1x = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
@@ -1646,10 +1328,11 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         const T r0 = add_rn(mul_rn(P.precess, c0x), mul_rn(P.damp, d0));
         const T r1 = add_rn(mul_rn(P.precess, c1x), mul_rn(P.damp, d1));
         const T r2 = add_rn(mul_rn(P.precess, c2x), mul_rn(P.damp, d2));
-        {
+        {   // maxTorqueRate: |rhs|^2 in double (dynamics.hpp:75-82)
             const double v0 = r0, v1 = r1, v2 = r2;
             tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
         }
+        // eulerUpdate (dynamics.hpp:93-121)
         T e0 = add_rn(mx, mul_rn(P.dt, r0));
         T e1 = add_rn(my, mul_rn(P.dt, r1));
         T e2 = add_rn(mz, mul_rn(P.dt, r2));
@@ -1700,34 +1383,18 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const long long nrows = (long long)g.ny * g.nz;
     const long long row0 = (long long)blockIdx.x * ROWS;
-    constexpr bool STG = CF::STG && !FWD;
-    constexpr int SROWS = CF::SROWS;
-    T* ms = reinterpret_cast<T*>(smem_raw + CF::SOFF);   // [3][SROWS][N]: rows row0-1 .. row0+ROWS
-    if constexpr (STG) {
-        constexpr int NV = N / V, NCH = 3 * SROWS * NV;   // 16-byte chunks (nx <= N)
-        const int nv = g.nx / V;
-#pragma unroll
-        for (int q0 = 0; q0 < NCH; q0 += NT) {
-            const int q = q0 + threadIdx.x;
-            const int c = q / (SROWS * NV), rr = (q / NV) % SROWS, v = q % NV;
-            const long long row = row0 - 1 + rr;
-            if ((NCH % NT == 0 || q < NCH) && v < nv && row >= 0 && row < nrows)
-                cp_async16(ms + (c * SROWS + rr) * N + v * V, M + c * g.ncell + row * g.nx + v * V);
-        }
-        cp_commit();
-    }
     if ((g.pfm & 6) && threadIdx.x < 3) {
         // this CTA's M rows with their y / z neighbour rows (read by the
         // epilogue, after the inverse FFT) ...
         const int c = threadIdx.x;
         if (g.pfm & 2) {
-        const T* Mc = M + c * g.ncell;
-        const long long nx = g.nx, ny = g.ny;
-        const long long ra = row0 - 1 > 0 ? row0 - 1 : 0, rb = row0 + ROWS + 1 < nrows ? row0 + ROWS + 1 : nrows;
-        l2_prefetch(Mc + ra * nx, (rb - ra) * nx * (long long)sizeof(T));
-        const long long re = row0 + ROWS < nrows ? row0 + ROWS : nrows;
-        if (row0 >= ny) l2_prefetch(Mc + (row0 - ny) * nx, (re - row0) * nx * (long long)sizeof(T));
-        if (re + ny <= nrows) l2_prefetch(Mc + (row0 + ny) * nx, (re - row0) * nx * (long long)sizeof(T));
+            const T* Mc = M + c * g.ncell;
+            const long long nx = g.nx, ny = g.ny;
+            const long long ra = row0 - 1 > 0 ? row0 - 1 : 0, rb = row0 + ROWS + 1 < nrows ? row0 + ROWS + 1 : nrows;
+            l2_prefetch(Mc + ra * nx, (rb - ra) * nx * (long long)sizeof(T));
+            const long long re = row0 + ROWS < nrows ? row0 + ROWS : nrows;
+            if (row0 >= ny) l2_prefetch(Mc + (row0 - ny) * nx, (re - row0) * nx * (long long)sizeof(T));
+            if (re + ny <= nrows) l2_prefetch(Mc + (row0 + ny) * nx, (re - row0) * nx * (long long)sizeof(T));
         }
         // ... and the spectrum rows of the CTA one resident wave later
         const long long r1 = row0 + (long long)g.pf5 * ROWS;
@@ -1739,8 +1406,9 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
     // C2R pre-process over pairs (k, N-k): item e -> (k = e % (N/2), column
     // = e / (N/2)); the k = 0 item also carries the self-paired k = N/2.  All
     // HBM loads of the thread are issued before any use (compile-time trip
-    // count) so the latency is paid once.  Z is written in natural order; the
-    // first inverse stage reads natural order.
+    // count) so the latency is paid once (measured faster than staging the
+    // rows in shared memory by cp.async first: 0.384 vs 0.395 ms at C4 f32).
+    // Z is written in natural order; the first inverse stage reads natural order.
     constexpr int HP = N / 2 > 0 ? N / 2 : 1;
     constexpr int ITEMS = NCOL * HP;
     constexpr int IT = (ITEMS + NT - 1) / NT;
@@ -1758,69 +1426,35 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
             scol[xpad<T>(N - k)] = mk<T>(s.x - wd.y, s.y + wd.x);
         }
     };
-    if constexpr (MFD_K5_ASYNC && N >= 2) {
-        // The CTA's NCOL spectrum rows (N+1 bins each) land in shared memory by
-        // cp.async at their padded positions (no staging registers: all of the
-        // CTA's HBM reads are in flight at once), then each thread turns its
-        // pairs (k, N-k) into the C2R input in place: a pair is read and written
-        // by one thread only, and bin N/2 / bin N belong to the k = 0 owner.
-        constexpr int RL = N + 1;
-        for (int e = threadIdx.x; e < NCOL * RL; e += NT) {
-            const int col = e / RL, k = e - (e / RL) * RL;
+    {
+        C2<T> pa[IT], pb[IT], pc[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * NT;
+            const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
             const long long row = row0 + col % ROWS;
-            C2<T>* d = sm + col * LP + xpad<T>(k);
-            if (row < nrows) cp_async_c2<T>(d, abin<MULTI>(g, A + ((long long)(col / ROWS) * nrows + row) * g.Hp, k));
-            else *d = mk<T>(0, 0);
-        }
-        cp_commit();
-        cp_wait<0>();
-        __syncthreads();
-#pragma unroll 4
-        for (int e = threadIdx.x; e < ITEMS; e += NT) {
-            const int col = e / HP, k = e - (e / HP) * HP;
-            C2<T>* scol = sm + col * LP;
-            const C2<T> a = scol[xpad<T>(k)], b = scol[xpad<T>(N - k)];
-            if (k == 0) {
-                const C2<T> c = scol[xpad<T>(N / 2)];
-                pre(scol, 0, a, b);
-                pre(scol, N / 2, c, c);
-            } else {
-                pre(scol, k, a, b);
+            pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
+            if (e < ITEMS && row < nrows) {
+                const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
+                pa[it] = *abin<MULTI>(g, src, k);
+                pb[it] = *abin<MULTI>(g, src, N - k);
+                if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, src, N / 2);
             }
         }
-    } else {
-    C2<T> pa[IT], pb[IT], pc[IT];
 #pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        const int e = threadIdx.x + it * NT;
-        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
-        const long long row = row0 + col % ROWS;
-        pa[it] = pb[it] = pc[it] = mk<T>(0, 0);
-        if (e < ITEMS && row < nrows) {
-            const C2<T>* src = A + ((long long)(col / ROWS) * nrows + row) * g.Hp;
-            pa[it] = *abin<MULTI>(g, src, k);
-            pb[it] = *abin<MULTI>(g, src, N - k);
-            if (k == 0 && N > 1) pc[it] = *abin<MULTI>(g, src, N / 2);
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * NT;
+            if (ITEMS % NT != 0 && e >= ITEMS) continue;
+            const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
+            pre(sm + col * LP, k, pa[it], pb[it]);
+            if (k == 0 && N > 1) pre(sm + col * LP, N / 2, pc[it], pc[it]);
         }
-    }
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-        const int e = threadIdx.x + it * NT;
-        if (ITEMS % NT != 0 && e >= ITEMS) continue;
-        const int col = e / HP, k = N / 2 > 0 ? e % HP : 0;
-        pre(sm + col * LP, k, pa[it], pb[it]);
-        if (k == 0 && N > 1) pre(sm + col * LP, N / 2, pc[it], pc[it]);
-    }
     }
     __syncthreads();
     if constexpr (Plan<T, N>::S > 0) {
         auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
         auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
         fft_inverse<T, N, NCOL, NT, false, true, true, true, true>(lds, lds, sts, sts, tw);
-        __syncthreads();
-    }
-    if constexpr (STG) {
-        cp_wait<0>();
         __syncthreads();
     }
     double tmax = 0;
@@ -1845,8 +1479,8 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
                 hd[c][q] = z.x * scale;
                 hd[c][q + 1] = z.y * scale;
             }
-        cells_vec<T, SUMS, STG>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
-                                FWD ? sm + r * LP : nullptr, ROWS * LP, ms + (r + 1) * N, SROWS * N, N);
+        cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
+                           FWD ? sm + r * LP : nullptr, ROWS * LP);
     }
     if constexpr (FWD && N >= 2) {
         // next step's K1 on the rows in shared memory (pairs beyond nx/2 are padding)

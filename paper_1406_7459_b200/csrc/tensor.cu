@@ -43,18 +43,6 @@ static PFN_cuTensorMapEncodeTiled tmap_encoder() {
     }
     return encode;
 }
-bool make_tmap_3d(CUtensorMap* map, const void* base, const unsigned long long dims[3],
-                  const unsigned long long strides_bytes[2], const unsigned box[3]) {
-    PFN_cuTensorMapEncodeTiled encode = tmap_encoder();
-    if (!encode) return false;
-    const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
-    const cuuint64_t st[2] = {strides_bytes[0], strides_bytes[1]};
-    const cuuint32_t b[3] = {box[0], box[1], box[2]};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), d, st, b, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 bool make_tmap_2d(CUtensorMap* map, const void* base, unsigned long long cols, unsigned long long rows,
                   unsigned long long pitch_bytes, unsigned box_cols, unsigned box_rows) {
     PFN_cuTensorMapEncodeTiled encode = tmap_encoder();

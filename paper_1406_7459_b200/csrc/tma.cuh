@@ -65,8 +65,5 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 // 8-byte elements with a row pitch of `pitch` elements; box = box_cols x box_rows.
 bool make_tmap_2d(CUtensorMap* map, const void* base, unsigned long long cols, unsigned long long rows,
                   unsigned long long pitch_bytes, unsigned box_cols, unsigned box_rows);
-// 3-D: dims d0 (contiguous, 8-byte elements), d1, d2; byte strides of d1, d2; box b0 x b1 x b2.
-bool make_tmap_3d(CUtensorMap* map, const void* base, const unsigned long long dims[3],
-                  const unsigned long long strides_bytes[2], const unsigned box[3]);
 
 } // namespace mfd
