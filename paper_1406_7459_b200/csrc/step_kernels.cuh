@@ -47,6 +47,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_Z2_W
 #define MFD_Z2_W 0             // K3 (two-stage) columns per CTA override (0: default)
 #endif
+#ifndef MFD_K3_KEARLY
+#define MFD_K3_KEARLY 1   // K3: first register phase's tensor loads issued during stage 0 (C4 f32 K3 0.539 -> 0.528 ms)
+#endif
 #ifndef MFD_YFWD_F64_MINB
 #define MFD_YFWD_F64_MINB 2   // f64 K2 (non-TMA y forward): 128 registers, 2 CTAs/SM (C4 f64 K2 0.713 -> 0.631 ms)
 #endif
@@ -709,6 +712,18 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     C2<T>* gcol = B + (long long)(r ? ybuf[vp] : ybuf[v]) * Wb + u0 + w;   // + comp*S_c + k*S_k
     // smem column of (comp c, row r, bin w): c*CO + r*W + w; layout [pos][NCOL]
     C2<T>* scol = sm + (SROW ? 0 : r * W) + w;
+    // tensor bins of the register phases (see stage 1 below)
+    const int Hz = L / 2 + 1;
+    const T sy = r ? T(-1) : T(1);
+    const T* kb = Kt + ((long long)v * Hz * Wb + u0 + w) * 6;
+    KBin<T> kv[CF::KPRE ? R1 : 1];
+    auto kfetch = [&](int it) {
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            const int f = n2 + R1 * it + R0 * k1;
+            kv[k1] = kload<T>(kb + (long long)(2 * f > L ? L - f : f) * Wb * 6);
+        }
+    };
     // ---- forward stage 0: x[R1*j + n2], j < R0/2 (upper half is padding).
     {
         // All three components' inputs go into flight at kernel entry as
@@ -737,6 +752,8 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
             if (c == 0) cp_wait<2>();
             else if (c == 1) cp_wait<1>();
             else cp_wait<0>();
+            // first phase's tensor bins in flight during the last component's DFT
+            if constexpr (CF::KPRE && MFD_K3_KEARLY) if (c == 2 && live) kfetch(0);
             C2<T> x[R0];
 #pragma unroll
             for (int j = 0; j < R0; ++j) x[j] = 2 * j < R0 ? scol[(R1 * j + n2) * NCOL + c * CO] : mk<T>(0, 0);
@@ -751,18 +768,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     // tensor bins of iteration it are loaded one phase ahead (before the
     // barrier for it = 0, after the product of it - 1 otherwise), so their
     // HBM latency overlaps the shared-memory gather and the stage-1 DFTs.
-    const int Hz = L / 2 + 1;
-    const T sy = r ? T(-1) : T(1);
-    const T* kb = Kt + ((long long)v * Hz * Wb + u0 + w) * 6;
-    KBin<T> kv[CF::KPRE ? R1 : 1];
-    auto kfetch = [&](int it) {
-#pragma unroll
-        for (int k1 = 0; k1 < R1; ++k1) {
-            const int f = n2 + R1 * it + R0 * k1;
-            kv[k1] = kload<T>(kb + (long long)(2 * f > L ? L - f : f) * Wb * 6);
-        }
-    };
-    if constexpr (CF::KPRE) if (live) kfetch(0);
+    if constexpr (CF::KPRE && !MFD_K3_KEARLY) if (live) kfetch(0);
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < R0 / R1; ++it) {
