@@ -268,7 +268,6 @@ void Engine<T>::init() {
     } else {
         k5_blocks_ = (n + 255) / 256;
     }
-    alloc(&partials_, (size_t)k5_blocks_ * 8 * sizeof(double));
     if (kYZSmall && terms_.demag && slab_.world == 1)
         with_yz([&]<int LY, int LZ>() {
             yz_small_ = true;
@@ -328,6 +327,8 @@ void Engine<T>::init() {
     if (const char* e = getenv("MFD_FUSE_K1"))   // A/B switch: 0 off, 2 on regardless of the grid size
         fuse_k1_ = atoi(e) == 2 ? (kFuseK1 && G == 1 && terms_.demag && geo_.N >= 2 && g.nx % V16<T>::V == 0)
                                 : fuse_k1_ && atoi(e) != 0;
+    // block_finish partials: one slot per CTA of a K5 launch
+    alloc(&partials_, (size_t)k5_blocks_ * 8 * sizeof(double));
     // Measured (single-row vs pair): f32 C4 0.609 -> 0.583 ms, C3 -12 %, C5 -14 %; f64 C4 1.18 -> 1.30 ms
     k3_srow_ = kK3SingleRow && sizeof(T) == 4;
     if (const char* e = getenv("MFD_K3_SROW")) k3_srow_ = atoi(e) != 0;   // A/B switch

@@ -190,17 +190,16 @@ __device__ __forceinline__ void r2c_post(const C2<T>* scol, C2<T>* dst, int k, C
 }
 
 // ------------------------------------------------------------------ K1
+// Body of one CTA (row group bx, component comp).
 template <class T, int N, int RS = 0, bool MULTI = false>
-__global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
-k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+__device__ __forceinline__ void k1_body(const Geo& g, const T* __restrict__ M, C2<T>* __restrict__ A,
+                                        const C2<T>* __restrict__ tw, long long bx, int comp,
+                                        unsigned char* smem_raw) {
     using CF = XCfg<T, N, RS>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>();
-    if (halted(ctl)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
-    const int comp = blockIdx.y;
     const long long nrows = (long long)g.ny * g.nz;
-    const long long row0 = (long long)blockIdx.x * ROWS;
+    const long long row0 = bx * ROWS;
     const T* Mc = M + comp * g.ncell;
     const int nx = g.nx;
     const bool even = (nx & 1) == 0;
@@ -268,6 +267,14 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
             if (k == 0 && N > 1) post(col, N / 2, __ldg(tw_dense<T, 2 * N>(tw) + N / 2));
         }
     }
+}
+
+template <class T, int N, int RS = 0, bool MULTI = false>
+__global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
+k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    k1_body<T, N, RS, MULTI>(g, M, A, tw, blockIdx.x, blockIdx.y, smem_raw);
 }
 
 // Measured on B200 (512x512x64 f32): the swizzle removes the conflicts but the
@@ -892,15 +899,13 @@ template <class T, int LY, int LZ> struct YZCfg {
 };
 
 template <class T, int LY, int LZ>
-__global__ void __launch_bounds__(YZCfg<T, LY, LZ>::NT)
-k_fft_yz_small(Geo g, C2<T>* __restrict__ A, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
-               const int* __restrict__ ybuf, Ctl ctl) {
+__device__ __forceinline__ void yz_body(const Geo& g, C2<T>* __restrict__ A, const T* __restrict__ Kt,
+                                        const C2<T>* __restrict__ tw, const int* __restrict__ ybuf, int bx,
+                                        unsigned char* smem_raw) {
     using CF = YZCfg<T, LY, LZ>;
     constexpr int W = CF::W, NZH = CF::NZH, NCOL = CF::NCOL, NT = CF::NT;
-    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);    // [y position][NCOL]
-    const int u0 = blockIdx.x * W;
+    const int u0 = bx * W;
     const int ny = g.ny, nz = g.nz, Hp = g.Hp;
     // column col = (comp * NZH + z) * W + w
     auto arow = [&](int col, int y) -> long long {
@@ -948,6 +953,15 @@ k_fft_yz_small(Geo g, C2<T>* __restrict__ A, const T* __restrict__ Kt, const C2<
         if (pos < ny && zok(col)) A[arow(col, pos)] = v;
     };
     fft_inverse<T, LY, NCOL, NT, true, true, false>(lds, lds, sts, stn, tw);
+}
+
+template <class T, int LY, int LZ>
+__global__ void __launch_bounds__(YZCfg<T, LY, LZ>::NT)
+k_fft_yz_small(Geo g, C2<T>* __restrict__ A, const T* __restrict__ Kt, const C2<T>* __restrict__ tw,
+               const int* __restrict__ ybuf, Ctl ctl) {
+    // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    yz_body<T, LY, LZ>(g, A, Kt, tw, ybuf, blockIdx.x, smem_raw);
 }
 
 // ------------------------------------------------------------------ K5
@@ -1250,6 +1264,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
                                           const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
                                           C2<T>* fsm = nullptr, int fstride = 0) {
     constexpr int V = V16<T>::V;
+    constexpr bool sums = SUMS;
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
     const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
     const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = kg > 0, hz1 = kg < g.nzg - 1;
@@ -1287,7 +1302,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             if (hz0) h = add_rn(h, mul_rn(P.cz, sub_rn(zm[q], mc)));
             if (hz1) h = add_rn(h, mul_rn(P.cz, sub_rn(zp[q], mc)));
             H[c][q] = add_rn(hd[c][q], h);
-            if (SUMS) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
+            if (sums) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
                 if (q < V - 1 || hx1) { const double e = (double)xp - mc; elink[q] += P.wx * e * e; }
                 if (hy1) { const double e = (double)yp[q] - mc; elink[q] += P.wy * e * e; }
                 if (hz1) { const double e = (double)zp[q] - mc; elink[q] += P.wz * e * e; }
@@ -1312,7 +1327,7 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             Hz = add_rn(Hz, P.hz);
         }
         if (io.write_h == 1) { H[0][q] = Hx; H[1][q] = Hy; H[2][q] = Hz; }
-        if (SUMS) {
+        if (sums) {
             acc[0] += (double)mx;
             acc[1] += (double)my;
             acc[2] += (double)mz;
@@ -1377,18 +1392,17 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
 // CTA consumed (only its own rows: no cross-CTA hazard).  Saves K1's M read
 // and launch on every step but the first of a graph chunk.
 template <class T, int N, bool SUMS, int RS = 0, bool FWD = false, bool MULTI = false>
-__global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
-k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
-              T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
-              Halo<T> hl) {
+__device__ __forceinline__ void k5_body(const Geo& g, C2<T>* __restrict__ A, const T* __restrict__ M,
+                                        T* __restrict__ Mn, T* __restrict__ Hout, const C2<T>* __restrict__ tw,
+                                        T scale, const LocalParams<T>& P, const StepIO& io, const Halo<T>& hl,
+                                        long long bx, unsigned char* smem_raw, double& tmax, double* acc, int& bad) {
+    constexpr bool fwd = FWD;
     using CF = LCfg<T, N, RS>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
     constexpr int V = V16<T>::V;
-    if (halted(ctl)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);
     const long long nrows = (long long)g.ny * g.nz;
-    const long long row0 = (long long)blockIdx.x * ROWS;
+    const long long row0 = bx * ROWS;
     if ((g.pfm & 6) && threadIdx.x < 3) {
         // this CTA's M rows with their y / z neighbour rows (read by the
         // epilogue, after the inverse FFT) ...
@@ -1463,9 +1477,6 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
         fft_inverse<T, N, NCOL, NT, false, true, true, true, true>(lds, lds, sts, sts, tw);
         __syncthreads();
     }
-    double tmax = 0;
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-    int bad = 0;
     const int nx = g.nx, nvec = nx / V;
     constexpr int EIT = (ROWS * (N / V) + NT - 1) / NT;   // nx <= N
 #pragma unroll
@@ -1486,7 +1497,7 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
                 hd[c][q + 1] = z.y * scale;
             }
         cells_vec<T, SUMS>(g, P, io, M, Mn, Hout, hl, row * nx + i0, i0, j, k, hd, tmax, acc, bad,
-                           FWD ? sm + r * LP : nullptr, ROWS * LP);
+                           fwd ? sm + r * LP : nullptr, ROWS * LP);
     }
     if constexpr (FWD && N >= 2) {
         // next step's K1 on the rows in shared memory (pairs beyond nx/2 are padding)
@@ -1507,7 +1518,20 @@ k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restri
             if (kk == 0) r2c_post<T, N>(sm + col * LP, dst, N / 2, __ldg(tw_dense<T, 2 * N>(tw) + N / 2));
         }
     }
-    block_finish<NT>(io, ctl, tmax, acc, bad);
+}
+
+template <class T, int N, bool SUMS, int RS = 0, bool FWD = false, bool MULTI = false>
+__global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
+k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
+              T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
+              Halo<T> hl) {
+    if (halted(ctl)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double tmax = 0;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int bad = 0;
+    k5_body<T, N, SUMS, RS, FWD, MULTI>(g, A, M, Mn, Hout, tw, scale, P, io, hl, blockIdx.x, smem_raw, tmax, acc, bad);
+    block_finish<LCfg<T, N, RS>::NT>(io, ctl, tmax, acc, bad);
 }
 
 // Demag-free step (terms.demag = false): H_eff from local terms only.
