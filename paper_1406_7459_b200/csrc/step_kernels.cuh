@@ -59,8 +59,22 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K5_F64_MINB
 #define MFD_K5_F64_MINB 2   // f64 K5: 128 registers, 2 CTAs/SM (C4 f64 K5 1.196 -> 0.949 ms despite a 144-byte spill)
 #endif
+#ifndef MFD_K5_F64_ROWS
+#define MFD_K5_F64_ROWS 2   // f64 K5: 2 rows per CTA (72 instead of 144 load registers): C4 f64 K5 0.960 -> 0.862 ms
+#endif
+#ifndef MFD_K5_F64_FMA
+#define MFD_K5_F64_FMA 1   // f64 K5 epilogue with FMA + rsqrt: C4 f64 K5 0.860 -> 0.843 ms
+#endif
+#ifndef MFD_Z2_F64_W
+#define MFD_Z2_F64_W 0      // f64 K3 columns per CTA override (0: default)
+#endif
+#ifndef MFD_K3_F64_KPRE
+#define MFD_K3_F64_KPRE 1   // f64 K3: tensor bins one register phase ahead
+#endif
 template <class T, int N, int RS = 0> struct LCfg {   // K5
-    static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(32, 2048 / cmax(N, 1)));
+    static constexpr int ROWS = RS > 0 ? RS
+                                       : (sizeof(T) == 8 && MFD_K5_F64_ROWS > 0 ? cmin(MFD_K5_F64_ROWS, cmax(1, cmin(32, 2048 / cmax(N, 1))))
+                                                                               : cmax(1, cmin(32, 2048 / cmax(N, 1))));
     static constexpr int NT = RS > 0 ? 64 : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
     static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
@@ -679,14 +693,16 @@ template <class T, int L, bool SROW = false> struct Z2Cfg {
     static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
     static constexpr int CS = sizeof(C2<T>);
     // f32: 16 columns (128-byte rows) also at R1 = 16 (Pz = 256, C5: 7.68 -> 7.07 ms)
-    static constexpr int W = MFD_Z2_W > 0 && sizeof(T) == 4 ? MFD_Z2_W : sizeof(T) == 4 ? 16 : 8 / (R1 >= 16 ? 2 : 1);
+    static constexpr int W = MFD_Z2_W > 0 && sizeof(T) == 4 ? MFD_Z2_W
+                             : sizeof(T) == 4 ? 16
+                             : MFD_Z2_F64_W > 0 ? MFD_Z2_F64_W : 8 / (R1 >= 16 ? 2 : 1);
     static constexpr int NROW = SROW ? 1 : 2;
     static constexpr int NCOL = 3 * NROW * W;
     static constexpr int NT = W * R1 * NROW;
     static constexpr int SMEM = NCOL * L * CS;
     // resident CTAs per SM the register budget is sized for (shared memory permitting)
     // tensor bins loaded one phase ahead (register budget: R1 <= 8 only)
-    static constexpr bool KPRE = R1 <= 8;
+    static constexpr bool KPRE = R1 <= 8 && (sizeof(T) == 4 || MFD_K3_F64_KPRE);
     // R1 = 16 (Pz = 256), f32: a 128-register budget for 2 CTAs/SM instead of
     // 254 registers at 1 CTA/SM (8 warps): C5 K3 7.14 -> 6.06 ms, C3 0.134 -> 0.121 ms
     static constexpr int MINB = KPRE ? cmax(1, cmin(2 * (3 - NROW), (200 * 1024) / SMEM))
@@ -1265,6 +1281,18 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
                                           C2<T>* fsm = nullptr, int fstride = 0) {
     constexpr int V = V16<T>::V;
     constexpr bool sums = SUMS;
+    // f64: fused multiply-adds and rsqrt in the epilogue (the f64 passes are
+    // FP64-issue-bound; the f32 epilogue measured faster in the strict form).
+    // The separate-rounding form stays in cell_update (the bitwise demag-free path).
+    constexpr bool FMA = sizeof(T) == 8 && MFD_K5_F64_FMA;
+    auto mad = [](T a, T b, T c) -> T {
+        if constexpr (FMA) return fma(a, b, c);
+        else return add_rn(mul_rn(a, b), c);
+    };
+    auto msub = [](T a, T b, T c) -> T {   // a*b - c
+        if constexpr (FMA) return fma(a, b, -c);
+        else return sub_rn(mul_rn(a, b), c);
+    };
     const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
     const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
     const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = kg > 0, hz1 = kg < g.nzg - 1;
@@ -1295,12 +1323,12 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
             const T mc = m[c][q];
             const T xm = q > 0 ? m[c][q - 1] : xl, xp = q < V - 1 ? m[c][q + 1] : xr;
             T h = 0;
-            if (q > 0 || hx0) h = add_rn(h, mul_rn(P.cx, sub_rn(xm, mc)));
-            if (q < V - 1 || hx1) h = add_rn(h, mul_rn(P.cx, sub_rn(xp, mc)));
-            if (hy0) h = add_rn(h, mul_rn(P.cy, sub_rn(ym[q], mc)));
-            if (hy1) h = add_rn(h, mul_rn(P.cy, sub_rn(yp[q], mc)));
-            if (hz0) h = add_rn(h, mul_rn(P.cz, sub_rn(zm[q], mc)));
-            if (hz1) h = add_rn(h, mul_rn(P.cz, sub_rn(zp[q], mc)));
+            if (q > 0 || hx0) h = mad(P.cx, sub_rn(xm, mc), h);
+            if (q < V - 1 || hx1) h = mad(P.cx, sub_rn(xp, mc), h);
+            if (hy0) h = mad(P.cy, sub_rn(ym[q], mc), h);
+            if (hy1) h = mad(P.cy, sub_rn(yp[q], mc), h);
+            if (hz0) h = mad(P.cz, sub_rn(zm[q], mc), h);
+            if (hz1) h = mad(P.cz, sub_rn(zp[q], mc), h);
             H[c][q] = add_rn(hd[c][q], h);
             if (sums) {   // exchange link energy, links to +x, +y, +z (fields.hpp:141-160)
                 if (q < V - 1 || hx1) { const double e = (double)xp - mc; elink[q] += P.wx * e * e; }
@@ -1340,29 +1368,29 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         }
         // llgRhs (dynamics.hpp:49-64): b = mu0 H, c = m x b, d = m x c, r = P c + D d
         const T b0 = mul_rn(P.mu0, Hx), b1 = mul_rn(P.mu0, Hy), b2 = mul_rn(P.mu0, Hz);
-        const T c0x = sub_rn(mul_rn(my, b2), mul_rn(mz, b1));
-        const T c1x = sub_rn(mul_rn(mz, b0), mul_rn(mx, b2));
-        const T c2x = sub_rn(mul_rn(mx, b1), mul_rn(my, b0));
-        const T d0 = sub_rn(mul_rn(my, c2x), mul_rn(mz, c1x));
-        const T d1 = sub_rn(mul_rn(mz, c0x), mul_rn(mx, c2x));
-        const T d2 = sub_rn(mul_rn(mx, c1x), mul_rn(my, c0x));
-        const T r0 = add_rn(mul_rn(P.precess, c0x), mul_rn(P.damp, d0));
-        const T r1 = add_rn(mul_rn(P.precess, c1x), mul_rn(P.damp, d1));
-        const T r2 = add_rn(mul_rn(P.precess, c2x), mul_rn(P.damp, d2));
+        const T c0x = msub(my, b2, mul_rn(mz, b1));
+        const T c1x = msub(mz, b0, mul_rn(mx, b2));
+        const T c2x = msub(mx, b1, mul_rn(my, b0));
+        const T d0 = msub(my, c2x, mul_rn(mz, c1x));
+        const T d1 = msub(mz, c0x, mul_rn(mx, c2x));
+        const T d2 = msub(mx, c1x, mul_rn(my, c0x));
+        const T r0 = mad(P.precess, c0x, mul_rn(P.damp, d0));
+        const T r1 = mad(P.precess, c1x, mul_rn(P.damp, d1));
+        const T r2 = mad(P.precess, c2x, mul_rn(P.damp, d2));
         {   // maxTorqueRate: |rhs|^2 in double (dynamics.hpp:75-82)
             const double v0 = r0, v1 = r1, v2 = r2;
             tmax = fmax(tmax, __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dmul_rn(v2, v2)));
         }
         // eulerUpdate (dynamics.hpp:93-121)
-        T e0 = add_rn(mx, mul_rn(P.dt, r0));
-        T e1 = add_rn(my, mul_rn(P.dt, r1));
-        T e2 = add_rn(mz, mul_rn(P.dt, r2));
+        T e0 = mad(P.dt, r0, mx);
+        T e1 = mad(P.dt, r1, my);
+        T e2 = mad(P.dt, r2, mz);
         if (io.renorm) {
             const T n2 = add_rn(add_rn(mul_rn(e0, e0), mul_rn(e1, e1)), mul_rn(e2, e2));
             if (!(n2 > T(0)) || !isfinite((double)n2)) {
                 all = false;
             } else {
-                const T f = P.Ms / sqrt(n2);
+                const T f = FMA ? mul_rn(P.Ms, rsqrt(n2)) : P.Ms / sqrt(n2);
                 e0 = mul_rn(f, e0); e1 = mul_rn(f, e1); e2 = mul_rn(f, e2);
             }
         } else if (!isfinite((double)add_rn(add_rn(e0, e1), e2))) {
