@@ -118,6 +118,14 @@ mfd_status mfd_set_m_f64(mfd_ctx* ctx, const double* mx, const double* my, const
 mfd_status mfd_get_m_f64(mfd_ctx* ctx, double* mx, double* my, double* mz);
 mfd_status mfd_set_m_f32(mfd_ctx* ctx, const float* mx, const float* my, const float* mz);
 mfd_status mfd_get_m_f32(mfd_ctx* ctx, float* mx, float* my, float* mz);
+/* Overlapped state upload: queue M from host memory on a copy stream and return at
+ * once; the next call that reads the state (step, step_async, relax, fields, get_m, ...)
+ * installs every queued state in order (the last one wins).  With pinned host arrays
+ * the transfer overlaps a step already enqueued by mfd_step_async (the arrays must stay
+ * untouched until the installing call returns); at most two states in flight.
+ * Pipelined use: stage(in_0); for each i: step_async(1); stage(in_{i+1}); sync_torque. */
+mfd_status mfd_stage_m_f64(mfd_ctx* ctx, const double* mx, const double* my, const double* mz);
+mfd_status mfd_stage_m_f32(mfd_ctx* ctx, const float* mx, const float* my, const float* mz);
 /* Uniform initial state M = Ms * dir (makeUniformState, state.hpp:71-78). */
 mfd_status mfd_set_m_uniform(mfd_ctx* ctx, const double dir[3]);
 
@@ -179,6 +187,8 @@ mfd_status mfd_step_async(mfd_ctx* ctx, long nsteps);
  * NULL) = the kernel launches those graphs contain. */
 mfd_status mfd_prepare_async(mfd_ctx* ctx, long nsteps, long* launches);
 mfd_status mfd_sync(mfd_ctx* ctx);
+/* mfd_sync + the pre-step max torque (deg/ns) of the last step of the last mfd_step_async. */
+mfd_status mfd_sync_torque(mfd_ctx* ctx, double* last_torque);
 /* The context's CUDA stream (cudaStream_t) for event timing. */
 void* mfd_stream(mfd_ctx* ctx);
 /* Kernel launches per step of the hot path (for bench accounting). */

@@ -97,6 +97,8 @@ def load_library() -> C.CDLL:
         "mfd_set_m_f32": (C.c_int, [V, _PF, _PF, _PF]),
         "mfd_get_m_f32": (C.c_int, [V, _PF, _PF, _PF]),
         "mfd_set_m_uniform": (C.c_int, [V, _PD]),
+        "mfd_stage_m_f64": (C.c_int, [V, _PD, _PD, _PD]),
+        "mfd_stage_m_f32": (C.c_int, [V, _PF, _PF, _PF]),
         "mfd_set_time": (C.c_int, [V, C.c_double, C.c_long]),
         "mfd_get_time": (C.c_int, [V, _PD, C.POINTER(C.c_long)]),
         "mfd_effective_field_f64": (C.c_int, [V, _PD, _PD, _PD]),
@@ -105,6 +107,7 @@ def load_library() -> C.CDLL:
         "mfd_step_async": (C.c_int, [V, C.c_long]),
         "mfd_prepare_async": (C.c_int, [V, C.c_long, C.POINTER(C.c_long)]),
         "mfd_sync": (C.c_int, [V]),
+        "mfd_sync_torque": (C.c_int, [V, _PD]),
         "mfd_stream": (V, [V]),
         "mfd_relax": (C.c_int, [V, C.POINTER(C.c_int), _SampleCB, V]),
         "mfd_sample_now": (C.c_int, [V, C.POINTER(_Sample)]),
@@ -279,6 +282,24 @@ class Simulation:
             x, y, z = (np.ascontiguousarray(m[i], dtype=np.float64) for i in range(3))
             self._check(self.lib.mfd_set_m_f64(self.h, _ptr(x), _ptr(y), _ptr(z)))
 
+    def stage_m(self, m: np.ndarray):
+        """Queue a new state (3 x N, float32 or float64) for the next step; the upload
+        overlaps a running step when m lives in pinned memory.  m must stay
+        untouched until the next call that reads the state returns."""
+        m = np.asarray(m).reshape(3, -1)
+        if m.shape[1] != self.n:
+            raise ValueError("stage_m: expected 3 x N values")
+        if m.dtype == np.float32:
+            if not m.flags.c_contiguous:
+                raise ValueError("stage_m: m must be C-contiguous")
+            self._check(self.lib.mfd_stage_m_f32(self.h, _ptr(m[0]), _ptr(m[1]), _ptr(m[2])))
+        else:
+            if m.dtype != np.float64 or not m.flags.c_contiguous:
+                raise ValueError("stage_m: m must be a C-contiguous float32 / float64 array")
+            self._check(self.lib.mfd_stage_m_f64(self.h, _ptr(m[0]), _ptr(m[1]), _ptr(m[2])))
+        # keep the host arrays of the (at most two) states in flight alive
+        self._staged = (getattr(self, "_staged", (None, None))[1], m)
+
     def get_m(self, dtype=np.float64) -> np.ndarray:
         out = np.zeros((3, self.n), dtype=dtype)
         x, y, z = out[0], out[1], out[2]
@@ -337,6 +358,12 @@ class Simulation:
 
     def sync(self):
         self._check(self.lib.mfd_sync(self.h))
+
+    def sync_torque(self) -> float:
+        """sync() + the pre-step torque (deg/ns) of the last asynchronous step."""
+        t = C.c_double()
+        self._check(self.lib.mfd_sync_torque(self.h, C.byref(t)))
+        return t.value
 
     def sample_now(self) -> Sample:
         s = _Sample()

@@ -127,6 +127,12 @@ mfd_status mfd_set_m_f32(mfd_ctx* c, const float* x, const float* y, const float
 mfd_status mfd_get_m_f32(mfd_ctx* c, float* x, float* y, float* z) {
     return guard(c, [&] { ENG(c)->get_m32(x, y, z); });
 }
+mfd_status mfd_stage_m_f64(mfd_ctx* c, const double* x, const double* y, const double* z) {
+    return guard(c, [&] { ENG(c)->stage_m(x, y, z, 64); });
+}
+mfd_status mfd_stage_m_f32(mfd_ctx* c, const float* x, const float* y, const float* z) {
+    return guard(c, [&] { ENG(c)->stage_m(x, y, z, 32); });
+}
 mfd_status mfd_set_m_uniform(mfd_ctx* c, const double dir[3]) {
     return guard(c, [&] {
         const double n = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
@@ -186,6 +192,9 @@ mfd_status mfd_prepare_async(mfd_ctx* c, long n, long* launches) {
     });
 }
 mfd_status mfd_sync(mfd_ctx* c) { return guard(c, [&] { ENG(c)->sync(); }); }
+mfd_status mfd_sync_torque(mfd_ctx* c, double* last_torque) {
+    return guard(c, [&] { *last_torque = ENG(c)->sync_torque(); });
+}
 void* mfd_stream(mfd_ctx* c) { return (void*)c->eng->stream(); }
 mfd_status mfd_relax(mfd_ctx* c, int* converged, mfd_sample_cb cb, void* user) {
     return guard(c, [&] { *converged = ENG(c)->relax(cb, user) ? 1 : 0; });

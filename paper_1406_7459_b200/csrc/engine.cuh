@@ -161,6 +161,9 @@ public:
     virtual ~EngineBase() = default;
     virtual void set_m(const double*, const double*, const double*) = 0;
     virtual void set_m32(const float*, const float*, const float*) = 0;
+    // Queue a new state from host memory on a copy stream (returns at once);
+    // the next state-reading call installs it.  f32 / f64 by the pointer type.
+    virtual void stage_m(const void* x, const void* y, const void* z, int bits) = 0;
     virtual void get_m(double*, double*, double*) = 0;
     virtual void get_m32(float*, float*, float*) = 0;
     virtual void set_uniform(const double dir[3]) = 0;
@@ -174,6 +177,8 @@ public:
     // returns the number of kernel launches those graphs contain.
     virtual long prepare_async(long n) = 0;
     virtual void sync() = 0;
+    // sync() + the pre-step max torque (deg/ns) of the last asynchronous step
+    virtual double sync_torque() = 0;
     virtual bool relax(mfd_sample_cb cb, void* user) = 0;
     virtual mfd_sample sample_now() = 0;
     virtual void timing(double ms[7]) = 0;
@@ -211,6 +216,7 @@ public:
 
     void set_m(const double* x, const double* y, const double* z) override;
     void set_m32(const float* x, const float* y, const float* z) override;
+    void stage_m(const void* x, const void* y, const void* z, int bits) override;
     void get_m(double* x, double* y, double* z) override;
     void get_m32(float* x, float* y, float* z) override;
     void set_uniform(const double dir[3]) override;
@@ -222,6 +228,8 @@ public:
     void step_async(long n) override;
     long prepare_async(long n) override;
     void sync() override;
+    double sync_torque() override;
+    int last_async_K_ = 0;                     // steps in the last step_async chunk
     bool relax(mfd_sample_cb cb, void* user) override;
     mfd_sample sample_now() override;
     void timing(double ms[7]) override;
@@ -280,6 +288,14 @@ private:
     double torque_of(unsigned long long bits) const;
     mfd_sample make_sample(const double sums[8], double torque) const;
     void eval(int write_h, bool sums, double& torque, double sum_out[8]);
+    // staged states (stage_m): device buffers filled on copy_stream_, installed
+    // into M_[cur_] by consume_staged() at the next state-reading call
+    void consume_staged();
+    cudaStream_t copy_stream_ = nullptr;
+    T* Mst_[2] = {nullptr, nullptr};
+    cudaEvent_t st_ready_[2] = {}, st_free_[2] = {};
+    int st_next_ = 0;
+    std::vector<int> st_pending_;              // FIFO of filled slots
     void ensure_stage() {
         if (!h_stage_) ck(cudaMallocHost((void**)&h_stage_, 3 * geo_.ncell * sizeof(T)), "host alloc");
     }

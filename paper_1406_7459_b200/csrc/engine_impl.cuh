@@ -382,6 +382,7 @@ void Engine<T>::release() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
     if (cstream_) cudaStreamSynchronize(cstream_);
+    if (copy_stream_) cudaStreamSynchronize(copy_stream_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     for (auto& a : allocs_) cudaFree(a.base);
     allocs_.clear();
@@ -393,6 +394,11 @@ void Engine<T>::release() {
     if (h_stage_) cudaFreeHost(h_stage_);
     for (auto& e : xev_)
         if (e) cudaEventDestroy(e);
+    for (int q = 0; q < 2; ++q) {
+        if (st_ready_[q]) cudaEventDestroy(st_ready_[q]);
+        if (st_free_[q]) cudaEventDestroy(st_free_[q]);
+    }
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (cstream_) cudaStreamDestroy(cstream_);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -924,6 +930,7 @@ static void copy3_d2h(const T* src, T* x, T* y, T* z, long long n, cudaStream_t 
 
 template <class T>
 void Engine<T>::set_m(const double* x, const double* y, const double* z) {
+    consume_staged();   // a later direct write wins over earlier staged states
     const long long n = geo_.ncell;
     if constexpr (std::is_same_v<T, double>) {
         copy3_h2d<T>(M_[cur_], x, y, z, n, stream_);
@@ -940,6 +947,7 @@ void Engine<T>::set_m(const double* x, const double* y, const double* z) {
 }
 template <class T>
 void Engine<T>::set_m32(const float* x, const float* y, const float* z) {
+    consume_staged();   // a later direct write wins over earlier staged states
     const long long n = geo_.ncell;
     if constexpr (std::is_same_v<T, float>) {
         copy3_h2d<T>(M_[cur_], x, y, z, n, stream_);
@@ -956,6 +964,7 @@ void Engine<T>::set_m32(const float* x, const float* y, const float* z) {
 }
 template <class T>
 void Engine<T>::get_m(double* x, double* y, double* z) {
+    consume_staged();
     const long long n = geo_.ncell;
     if constexpr (std::is_same_v<T, double>) {
         copy3_d2h<T>(M_[cur_], x, y, z, n, stream_);
@@ -972,6 +981,7 @@ void Engine<T>::get_m(double* x, double* y, double* z) {
 }
 template <class T>
 void Engine<T>::get_m32(float* x, float* y, float* z) {
+    consume_staged();
     const long long n = geo_.ncell;
     if constexpr (std::is_same_v<T, float>) {
         copy3_d2h<T>(M_[cur_], x, y, z, n, stream_);
@@ -986,8 +996,55 @@ void Engine<T>::get_m32(float* x, float* y, float* z) {
         z[i] = (float)h_stage_[i + 2 * n];
     }
 }
+// Overlapped state upload: the host arrays (pinned for a true async copy; they
+// must stay untouched until the next call that reads the state returns) go to
+// a device staging buffer on a copy stream, so the transfer of the next
+// step's state overlaps the current step; two slots in flight at most.
+template <class T>
+void Engine<T>::stage_m(const void* x, const void* y, const void* z, int bits) {
+    if (bits != (int)(8 * sizeof(T))) {   // other precision: converting copy, synchronous
+        consume_staged();
+        if (bits == 32) set_m32((const float*)x, (const float*)y, (const float*)z);
+        else set_m((const double*)x, (const double*)y, (const double*)z);
+        return;
+    }
+    const long long n = geo_.ncell;
+    if (!copy_stream_) {
+        ck(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "stream");
+        for (int s = 0; s < 2; ++s) {
+            Mst_[s] = static_cast<T*>(dalloc(3 * n * sizeof(T)));
+            ck(cudaEventCreateWithFlags(&st_ready_[s], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&st_free_[s], cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(st_free_[s], stream_), "event");
+        }
+    }
+    if ((int)st_pending_.size() == 2) consume_staged();   // at most two states in flight
+    const int s = st_next_;
+    st_next_ ^= 1;
+    ck(cudaStreamWaitEvent(copy_stream_, st_free_[s], 0), "wait");   // its previous install is done
+    ck(cudaMemcpyAsync(Mst_[s], x, n * sizeof(T), cudaMemcpyHostToDevice, copy_stream_), "h2d");
+    ck(cudaMemcpyAsync(Mst_[s] + n, y, n * sizeof(T), cudaMemcpyHostToDevice, copy_stream_), "h2d");
+    ck(cudaMemcpyAsync(Mst_[s] + 2 * n, z, n * sizeof(T), cudaMemcpyHostToDevice, copy_stream_), "h2d");
+    ck(cudaEventRecord(st_ready_[s], copy_stream_), "event");
+    st_pending_.push_back(s);
+}
+
+// Install the oldest staged state (if any) into M_[cur_], in stream order.
+template <class T>
+void Engine<T>::consume_staged() {
+    while (!st_pending_.empty()) {
+        const int s = st_pending_.front();
+        st_pending_.erase(st_pending_.begin());
+        ck(cudaStreamWaitEvent(stream_, st_ready_[s], 0), "wait");
+        ck(cudaMemcpyAsync(M_[cur_], Mst_[s], 3 * geo_.ncell * sizeof(T), cudaMemcpyDeviceToDevice, stream_), "d2d");
+        ck(cudaEventRecord(st_free_[s], stream_), "event");
+        if (!st_pending_.empty()) continue;   // a later staged state supersedes this one
+    }
+}
+
 template <class T>
 void Engine<T>::set_uniform(const double dir[3]) {
+    consume_staged();   // a later direct write wins over earlier staged states
     // makeUniformState: (Ms * direction).cast<T>() (state.hpp:71-78)
     const double Ms = mat_.Ms;
     k_fill3<T><<<(unsigned)((geo_.ncell + 255) / 256), 256, 0, stream_>>>(
@@ -998,6 +1055,7 @@ void Engine<T>::set_uniform(const double dir[3]) {
 
 template <class T>
 void Engine<T>::set_vortex(int axis) {
+    consume_staged();   // a later direct write wins over earlier staged states
     static const double av[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
     if (axis < 0 || axis > 5) throw Error(MFD_EINVAL, "axisVector: bad axis");
     const double* a = av[axis];
@@ -1016,6 +1074,7 @@ void Engine<T>::set_vortex(int axis) {
 // One evaluation without update (H, torque and optionally the sample sums).
 template <class T>
 void Engine<T>::eval(int write_h, bool sums, double& torque, double sum_out[8]) {
+    consume_staged();
     Iter it;
     it.update = 0;
     it.renorm = 0;
@@ -1082,6 +1141,7 @@ void Engine<T>::set_stepper(const mfd_stepper& s) {
 // Simulation<T>::step x n: renormalise iff (step+1) % renormalizeEvery == 0 (sim.hpp:38).
 template <class T>
 void Engine<T>::step(long n, double* last, double* all) {
+    consume_staged();
     long done = 0;
     std::vector<double> tq;
     while (done < n) {
@@ -1140,6 +1200,7 @@ long Engine<T>::prepare_async(long n) {
 
 template <class T>
 void Engine<T>::step_async(long n) {
+    consume_staged();
     // Benchmark path: whole graphs of 64 steps, no host round trip; the
     // renormalisation pattern is fixed per graph.  The host clock advances
     // optimistically; each chunk's error word is copied out behind it, so
@@ -1150,6 +1211,7 @@ void Engine<T>::step_async(long n) {
         const std::vector<Iter> its = async_chunk(K, stepno);
         if ((int)pending_.size() == kMaxPending) sync();
         run_chunk(its, cur_);
+        last_async_K_ = K;
         ck(cudaMemcpyAsync(h_perr_ + pending_.size(), err_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
         pending_.push_back(Pending{K, stepno, t, cur_});
         for (int i = 0; i < K; ++i) {
@@ -1186,6 +1248,15 @@ void Engine<T>::sync() {
 }
 
 template <class T>
+double Engine<T>::sync_torque() {
+    sync();
+    if (last_async_K_ <= 0) throw Error(MFD_EINVAL, "sync_torque: no asynchronous step has run");
+    unsigned long long bits = 0;
+    ck(cudaMemcpy(&bits, torque_ + last_async_K_ - 1, sizeof bits, cudaMemcpyDeviceToHost), "d2h");
+    return torque_of(bits);
+}
+
+template <class T>
 mfd_sample Engine<T>::make_sample(const double s[8], double torque) const {
     // reducedMean (state.hpp:113-124) + energies (fields.hpp:127-190) from the device sums
     mfd_sample o{};
@@ -1219,6 +1290,7 @@ mfd_sample Engine<T>::sample_now() {
 // (iter % sampleEvery == 0) reduce <m> and the energies inside K5.
 template <class T>
 bool Engine<T>::relax(mfd_sample_cb cb, void* user) {
+    consume_staged();
     if (!(st_.dt > 0)) throw Error(MFD_EINVAL, "StepperConfig: dt must be > 0");
     const long startStep = stepno;
     long iter = 0;
@@ -1297,6 +1369,7 @@ void Engine<T>::debug_stage(int stage, double* out) {
 
 template <class T>
 void Engine<T>::timing(double ms[7]) {
+    consume_staged();
     // One real Simulation::step with an event after every pass (advances the state).
     // The pass boundaries are event-record nodes of a captured one-iteration
     // graph, so the passes run exactly as inside the step graphs.

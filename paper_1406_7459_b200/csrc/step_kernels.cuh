@@ -1273,12 +1273,14 @@ __device__ __forceinline__ void vstore(T* p, const T* in) {
 // with separate round-to-nearest multiplies and adds as the reference build
 // (no FMA).  fsm (fused next-step x pass): the new M of the V cells also goes
 // to shared memory as (x[2n], x[2n+1]) pairs at component stride fstride.
-template <class T, bool SUMS>
-__device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
-                                          const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
-                                          const Halo<T>& hl, long long c0, int i0, int j, int k,
-                                          const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
-                                          C2<T>* fsm = nullptr, int fstride = 0) {
+// The per-vector arithmetic, independent of where M and its neighbours live:
+// Acc supplies the loads (m, ym, yp, zm, zp as V-vectors; xl, xr scalars) and
+// the stores of H and the new M; nb = {hx0, hx1, hy0, hy1, hz0, hz1} says
+// which neighbours exist (Neumann boundaries).
+template <class T, bool SUMS, class Acc>
+__device__ __forceinline__ void cells_core(const Acc& ac, const LocalParams<T>& P, const StepIO& io,
+                                           const bool (&nb)[6], const T (&hd)[3][V16<T>::V], double& tmax,
+                                           double* acc, int& bad, C2<T>* fsm, int fstride, int i0) {
     constexpr int V = V16<T>::V;
     constexpr bool sums = SUMS;
     // f64: fused multiply-adds and rsqrt in the epilogue (the f64 passes are
@@ -1293,31 +1295,26 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
         if constexpr (FMA) return fma(a, b, -c);
         else return sub_rn(mul_rn(a, b), c);
     };
-    const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
-    const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
-    const bool hy0 = j > 0, hy1 = j < g.ny - 1, hz0 = kg > 0, hz1 = kg < g.nzg - 1;
-    const bool hx0 = i0 > 0, hx1 = i0 + V < g.nx;
-    const long long inplane = c0 - (long long)k * sz;  // j*nx + i0
+    const bool hx0 = nb[0], hx1 = nb[1], hy0 = nb[2], hy1 = nb[3], hz0 = nb[4], hz1 = nb[5];
     T m[3][V], H[3][V];
     double elink[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) elink[q] = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const T* p = M + c * n + c0;
-        vload<T>(p, m[c]);
+        ac.m(c, m[c]);
         if (!P.exch) {
 #pragma unroll
             for (int q = 0; q < V; ++q) H[c][q] = hd[c][q];
             continue;
         }
         T ym[V], yp[V], zm[V], zp[V];
-        if (hz0) vload<T>(k > 0 ? p - sz : hl.lo + c * sz + inplane, zm);          // slab edge: halo plane
-        if (hz1) vload<T>(k < g.nz - 1 ? p + sz : hl.hi + c * sz + inplane, zp);
-        if (hy0) vload<T>(p - sy, ym);
-        if (hy1) vload<T>(p + sy, yp);
-        const T xl = hx0 ? __ldg(p - 1) : T(0);
-        const T xr = hx1 ? __ldg(p + V) : T(0);
+        if (hz0) ac.zm(c, zm);
+        if (hz1) ac.zp(c, zp);
+        if (hy0) ac.ym(c, ym);
+        if (hy1) ac.yp(c, yp);
+        const T xl = hx0 ? ac.xl(c) : T(0);
+        const T xr = hx1 ? ac.xr(c) : T(0);
 #pragma unroll
         for (int q = 0; q < V; ++q) {
             const T mc = m[c][q];
@@ -1400,12 +1397,12 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
     }
     if (io.write_h) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) vstore<T>(Hout + c * n + c0, io.write_h == 1 ? H[c] : hd[c]);
+        for (int c = 0; c < 3; ++c) ac.store_h(c, io.write_h == 1 ? H[c] : hd[c]);
     }
     if (io.update) {
         if (!all) bad = 1;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) vstore<T>(Mn + c * n + c0, mo[c]);
+        for (int c = 0; c < 3; ++c) ac.store_m(c, mo[c]);
         if (fsm) {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
@@ -1413,6 +1410,54 @@ __device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P,
                 for (int q = 0; q < V; q += 2) fsm[c * fstride + xpad<T>((i0 + q) >> 1)] = mk<T>(mo[c][q], mo[c][q + 1]);
         }
     }
+}
+
+// Global-memory accessor of cells_core: M / Mn / Hout are SoA lattices, the
+// z neighbours of a slab's edge planes come from the halo planes.
+template <class T>
+struct GAcc {
+    static constexpr int V = V16<T>::V;
+    const T* p;              // M + c0 (component 0)
+    T* mn;                   // Mn + c0
+    T* h;                    // Hout + c0
+    long long n, sy, sz;
+    const T* zlo;            // component-0 address of the z- neighbour vector
+    const T* zhi;
+    long long zlo_cs, zhi_cs;   // their component strides
+    __device__ __forceinline__ void m(int c, T* o) const { vload<T>(p + c * n, o); }
+    __device__ __forceinline__ void ym(int c, T* o) const { vload<T>(p + c * n - sy, o); }
+    __device__ __forceinline__ void yp(int c, T* o) const { vload<T>(p + c * n + sy, o); }
+    __device__ __forceinline__ void zm(int c, T* o) const { vload<T>(zlo + c * zlo_cs, o); }
+    __device__ __forceinline__ void zp(int c, T* o) const { vload<T>(zhi + c * zhi_cs, o); }
+    __device__ __forceinline__ T xl(int c) const { return __ldg(p + c * n - 1); }
+    __device__ __forceinline__ T xr(int c) const { return __ldg(p + c * n + V); }
+    __device__ __forceinline__ void store_h(int c, const T* v) const { vstore<T>(h + c * n, v); }
+    __device__ __forceinline__ void store_m(int c, const T* v) const { vstore<T>(mn + c * n, v); }
+};
+
+template <class T, bool SUMS>
+__device__ __forceinline__ void cells_vec(const Geo& g, const LocalParams<T>& P, const StepIO& io,
+                                          const T* __restrict__ M, T* __restrict__ Mn, T* __restrict__ Hout,
+                                          const Halo<T>& hl, long long c0, int i0, int j, int k,
+                                          const T (&hd)[3][V16<T>::V], double& tmax, double* acc, int& bad,
+                                          C2<T>* fsm = nullptr, int fstride = 0) {
+    constexpr int V = V16<T>::V;
+    const long long n = g.ncell, sy = g.nx, sz = (long long)g.nx * g.ny;
+    const int kg = g.k0 + k;                         // global plane: Neumann boundaries are global
+    const long long inplane = c0 - (long long)k * sz;  // j*nx + i0
+    const bool nb[6] = {i0 > 0, i0 + V < g.nx, j > 0, j < g.ny - 1, kg > 0, kg < g.nzg - 1};
+    GAcc<T> ac;
+    ac.p = M + c0;
+    ac.mn = Mn + c0;
+    ac.h = Hout + c0;
+    ac.n = n;
+    ac.sy = sy;
+    ac.sz = sz;
+    ac.zlo = k > 0 ? M + c0 - sz : hl.lo + inplane;            // slab edge: halo plane
+    ac.zhi = k < g.nz - 1 ? M + c0 + sz : hl.hi + inplane;
+    ac.zlo_cs = k > 0 ? n : sz;
+    ac.zhi_cs = k < g.nz - 1 ? n : sz;
+    cells_core<T, SUMS>(ac, P, io, nb, hd, tmax, acc, bad, fsm, fstride, i0);
 }
 
 // FWD: also run the NEXT step's x pass (K1) on the new M of this CTA's rows

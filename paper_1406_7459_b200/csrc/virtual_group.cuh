@@ -62,6 +62,10 @@ public:
             e->get_m32(x + o, y + o, z + o);
         }
     }
+    void stage_m(const void* x, const void* y, const void* z, int bits) override {
+        if (bits == 32) set_m32((const float*)x, (const float*)y, (const float*)z);
+        else set_m((const double*)x, (const double*)y, (const double*)z);
+    }
     void set_uniform(const double dir[3]) override {
         for (auto& e : ranks_) e->set_uniform(dir);
     }
@@ -122,6 +126,7 @@ public:
         return n * world_ * (long)ranks_[0]->launches_per_step();   // eager: no graphs
     }
     void sync() override { ck(cudaStreamSynchronize(stream_), "sync"); }
+    double sync_torque() override { throw Error(MFD_EINVAL, "sync_torque: single-GPU / one-process-per-GPU contexts only"); }
 
     bool relax(mfd_sample_cb cb, void* user) override {
         const long startStep = stepno;

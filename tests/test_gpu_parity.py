@@ -292,3 +292,28 @@ def test_step_async_error_rolls_back_clock():
     assert sim.time()[1] == n_ok
     assert np.all(np.isfinite(sim.get_m()))
     sim.sync()   # error consumed
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_staged_upload_pipeline_equals_serial(prec):
+    """mfd_stage_m (overlapped H2D on a copy stream) + step_async + sync_torque gives
+    bitwise the states and torques of set_m + step; staging twice installs the last."""
+    s = spec_of((33, 17, 5, 2e-9, 2e-9, 3e-9), alpha=0.1)
+    dt = np.float32 if prec == 32 else np.float64
+    ins = [O.random_unit_field(s.n, MS, 40 + i).astype(dt) for i in range(4)]
+    a, b = engine_sim(s, prec), engine_sim(s, prec)
+    ta, tb = [], []
+    for m in ins:
+        a.set_m(m)
+        ta.append(a.step(1))
+    b.stage_m(ins[0])
+    for i in range(len(ins)):
+        b.step_async(1)
+        if i + 1 < len(ins):
+            b.stage_m(ins[i + 1])
+        tb.append(b.sync_torque())
+    assert ta == tb
+    assert np.array_equal(a.get_m(dt), b.get_m(dt))
+    b.stage_m(ins[1])
+    b.stage_m(ins[2])                       # the later staged state wins
+    assert np.array_equal(b.get_m(dt), ins[2])
