@@ -283,8 +283,11 @@ __device__ __forceinline__ void k1_body(const Geo& g, const T* __restrict__ M, C
     }
 }
 
+#ifndef MFD_K1_MINB
+#define MFD_K1_MINB 0   // f32 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
+#endif
 template <class T, int N, int RS = 0, bool MULTI = false>
-__global__ void __launch_bounds__(XCfg<T, N, RS>::NT)
+__global__ void __launch_bounds__(XCfg<T, N, RS>::NT, (sizeof(T) == 4 && RS == 0 && MFD_K1_MINB > 0) ? MFD_K1_MINB : 1)
 k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
