@@ -1037,8 +1037,7 @@ void Engine<T>::consume_staged() {
         st_pending_.erase(st_pending_.begin());
         ck(cudaStreamWaitEvent(stream_, st_ready_[s], 0), "wait");
         ck(cudaMemcpyAsync(M_[cur_], Mst_[s], 3 * geo_.ncell * sizeof(T), cudaMemcpyDeviceToDevice, stream_), "d2d");
-        ck(cudaEventRecord(st_free_[s], stream_), "event");
-        if (!st_pending_.empty()) continue;   // a later staged state supersedes this one
+        ck(cudaEventRecord(st_free_[s], stream_), "event");   // a later staged state overwrites this one
     }
 }
 

@@ -32,9 +32,14 @@ template <class T, int L> constexpr int xpitch() { return L + (L >> padShift<T>(
 // -------------------------------------------------------------- configs
 // RS > 0: small-grid variant with RS rows per CTA, so grids of a few dozen
 // rows (SP4: 32) still spread over the SMs instead of running 1-3 CTAs.
+#ifndef MFD_K1_F64_ROWS
+#define MFD_K1_F64_ROWS 0   // f64 K1 rows per CTA override (0: the formula below)
+#endif
 template <class T, int N, int RS = 0> struct XCfg {   // K1
     static constexpr int E = regE<T>();
-    static constexpr int ROWS = RS > 0 ? RS : cmax(1, cmin(64, 128 * E / N));   // small CTAs: many phase schedules per SM
+    static constexpr int ROWS = RS > 0                                ? RS
+                                : sizeof(T) == 8 && MFD_K1_F64_ROWS > 0 ? MFD_K1_F64_ROWS
+                                                                      : cmax(1, cmin(64, 128 * E / N));   // small CTAs: many phase schedules per SM
     static constexpr int NT = RS > 0 ? clampNT(ROWS * N / E) : clampNT(cmax(128, ROWS * N / E));
     static constexpr int SMEM = ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
 };
@@ -363,16 +368,21 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
 // buffer (cp.async.bulk.tensor, mbarrier-completed) while the current tile runs
 // its second FFT stage, so no warp waits on global loads.  Same arithmetic as
 // k_fft_y_fwd.
+#ifndef MFD_K2_TMA3
+#define MFD_K2_TMA3 1   // TMA-staged K2 also for three-stage plans (f32 Py = 2048, f64 Py = 1024)
+#endif
 template <class T, int L> struct YTCfg {
     static constexpr int W = YCfg<T, L>::W, NT = YCfg<T, L>::NT, CS = sizeof(C2<T>);
     static constexpr int SMEM = W * L * CS + W * (L / 2) * CS + 128;   // work + staging (ny <= L/2 rows) + align
+    static constexpr int MINB = 2 * SMEM <= 220 * 1024 ? 2 : 1;
     // Measured (f32): Py = 1024 0.317 -> 0.243 ms (512x512x64); at Py = 256 the
     // plain kernel is ~10 % faster (short tiles), so staging starts at 512
-    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 110 * 1024 && L >= 512;
+    static constexpr bool OK = (Plan<T, L>::S == 2 && SMEM <= 110 * 1024 && L >= 512) ||
+                               (MFD_K2_TMA3 && Plan<T, L>::S == 3 && SMEM <= 220 * 1024);
 };
 
 template <class T, int L, bool FY>
-__global__ void __launch_bounds__(YTCfg<T, L>::NT, 2)
+__global__ void __launch_bounds__(YTCfg<T, L>::NT, YTCfg<T, L>::MINB)
 k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restrict__ B,
                 const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int box_rows, int comp0, int ncomp) {
     using CF = YTCfg<T, L>;
@@ -424,7 +434,13 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
             fence_proxy_async_smem();
             issue(t + gridDim.x);
         }
-        fft_stage<T, L, 1, false, W, NT, true, false, false, false, false, TWL>(lds, stn, tw);
+        if constexpr (Plan<T, L>::S == 3) {
+            fft_stage<T, L, 1, false, W, NT, true, true, false, false, false, TWL>(lds, sts, tw);
+            __syncthreads();
+            fft_stage<T, L, 2, false, W, NT, true, false, false, false, false, TWL>(lds, stn, tw);
+        } else {
+            fft_stage<T, L, 1, false, W, NT, true, false, false, false, false, TWL>(lds, stn, tw);
+        }
         __syncthreads();   // work buffer free for the next tile
     }
 }
@@ -465,9 +481,13 @@ k_fft_y_inv(Geo g, const C2<T>* __restrict__ B, C2<T>* __restrict__ A, const C2<
 // never share a bank wavefront (with 64-byte rows the tasks, R1 rows apart,
 // collide 2-way and TMA destinations cannot be padded off the 128-byte grid).
 // Same arithmetic as k_fft_y_inv.
+#ifndef MFD_K4_TMA3
+#define MFD_K4_TMA3 1   // TMA-staged K4 also for three-stage plans (f32 Py = 2048, f64 Py = 1024)
+#endif
 template <class T, int L> struct YICfg {
     static constexpr int CS = sizeof(C2<T>);
-    static constexpr int W = 128 / CS;                        // 128-byte tile rows
+    // 128-byte tile rows; 64-byte rows where three 128-byte half-tile slots exceed 200 KB (f32 Py = 2048)
+    static constexpr int W = (3 * (L / 2) * 128 <= 200 * 1024 ? 128 : 64) / CS;
     static constexpr int NT = clampNT(W * L / regE<T>());
     static constexpr int MINB = NT >= 512 ? 1 : 2;
     static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
@@ -476,7 +496,8 @@ template <class T, int L> struct YICfg {
     static constexpr int SLOT = SLOTE * CS;                   // bytes per slot
     static constexpr int BOX = HALF < 256 ? HALF : 256;       // TMA box rows (<= 256)
     static constexpr int SMEM = 3 * SLOT + 128;               // + TMA alignment
-    static constexpr bool OK = Plan<T, L>::S == 2 && SMEM <= 200 * 1024 && L >= 256;
+    static constexpr bool OK = (Plan<T, L>::S == 2 || (MFD_K4_TMA3 && Plan<T, L>::S == 3)) && SMEM <= 200 * 1024 &&
+                               L >= 256;
 };
 
 template <class T, int L, bool FY>
@@ -527,7 +548,21 @@ k_fft_y_inv_tma(Geo g, const __grid_constant__ CUtensorMap tmB, C2<T>* __restric
         mbar_wait(&bar[(2 * i + 1) % 3], ((2 * i + 1) / 3) & 1);
         // transposed stage 1 (MP = 1, no twiddles): task p owns rows p*R1 ..
         // p*R1+R1-1, all in one slot; in place, so no barrier between gather and scatter
-        {
+        if constexpr (Plan<T, L>::S == 3) {
+            // three-stage plans: the transposed stages 2 (MP = 1) and 1 (MP = R2)
+            // through the generic stage over the two slots; every task scatters to
+            // the positions it gathered, so both run in place without a mid barrier
+            auto lds = [&](int col, int pos) -> C2<T> {
+                return pos < HALF ? sa[pos * W + col] : sb[(pos - HALF) * W + col];
+            };
+            auto sts = [&](int col, int pos, C2<T> v) {
+                if (pos < HALF) sa[pos * W + col] = v;
+                else sb[(pos - HALF) * W + col] = v;
+            };
+            fft_stage<T, L, 2, true, W, NT, true, false>(lds, sts, tw);
+            __syncthreads();
+            fft_stage<T, L, 1, true, W, NT, true, false>(lds, sts, tw);
+        } else {
             constexpr int TPT1 = (W * R0 + NT - 1) / NT;
             static_assert((W * R0) % NT == 0 && R0 * R1 == L, "two-stage plan, whole tasks per thread");
 #pragma unroll
@@ -692,8 +727,15 @@ __device__ __forceinline__ void kmul(C2<T>& mx, C2<T>& my, C2<T>& mz, const T* _
 // SROW: one y row per CTA (the CTAs of rows v and Py-v are launched next to
 // each other, so the second one's tensor bins come from L2) instead of the
 // pair {v, Py-v}: half the shared memory and threads, twice the CTAs per SM.
+#ifndef MFD_K3_R1_256
+// f32 K3 at Pz = 256: radix 32 x 8 instead of the shared plan's 16 x 16 (stage 1 as at
+// Pz = 128, tensor bins prefetched; 128 threads, 252 registers, 2 CTAs/SM):
+// C5 K3 5.69 -> 5.35 ms, C3 0.113 -> 0.108 ms.  0: the shared plan
+#define MFD_K3_R1_256 8
+#endif
 template <class T, int L, bool SROW = false> struct Z2Cfg {
-    static constexpr int R0 = Plan<T, L>::R0, R1 = Plan<T, L>::R1;
+    static constexpr int R1 = sizeof(T) == 4 && L == 256 && MFD_K3_R1_256 > 0 ? MFD_K3_R1_256 : Plan<T, L>::R1;
+    static constexpr int R0 = L / R1;
     static constexpr int CS = sizeof(C2<T>);
     // f32: 16 columns (128-byte rows) also at R1 = 16 (Pz = 256, C5: 7.68 -> 7.07 ms)
     static constexpr int W = MFD_Z2_W > 0 && sizeof(T) == 4 ? MFD_Z2_W
@@ -721,7 +763,7 @@ k_fft_z_conv2(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const C2<T
     using CF = Z2Cfg<T, L, SROW>;
     constexpr int W = CF::W, NCOL = CF::NCOL, R0 = CF::R0, R1 = CF::R1;
     constexpr int CO = CF::NROW * W;   // column stride of the components
-    static_assert(Plan<T, L>::S == 2 && R0 % R1 == 0, "two-stage plans with R0 % R1 == 0 only");
+    static_assert(Plan<T, L>::S == 2 && R0 % R1 == 0 && R0 <= 32, "two-stage plans with R0 % R1 == 0 only");
     // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smem_raw);

@@ -32,6 +32,8 @@ SIZE_GRIDS = [
     (4, 512, 2, 1e-9, 1e-9, 1e-9), (2, 1024, 1, 1e-9, 1e-9, 1e-9),
     (2, 2, 256, 1e-9, 1e-9, 1e-9), (2, 3, 1024, 1e-9, 1e-9, 1e-9),
     (64, 48, 40, 2e-9, 2e-9, 2e-9), (200, 100, 3, 2e-9, 2e-9, 2e-9),
+    (20, 12, 100, 2e-9, 2e-9, 1e-9),                # Pz = 256 with nz < Pz/2 (K3 non-FZ, radix 32 x 8)
+    (3, 768, 1, 1e-9, 1e-9, 1e-9),                  # Py = 2048 with ny < Py/2 (three-stage TMA K2, FY=0)
 ]
 
 
@@ -317,3 +319,45 @@ def test_staged_upload_pipeline_equals_serial(prec):
     b.stage_m(ins[1])
     b.stage_m(ins[2])                       # the later staged state wins
     assert np.array_equal(b.get_m(dt), ins[2])
+
+
+def test_set_stepper_equals_fresh_context():
+    """mfd_set_stepper on a live context (captured graphs dropped) == a context built with it."""
+    import paper_1406_7459_b200 as E
+    s1 = spec_of((16, 8, 4, 3e-9, 2e-9, 1e-9), dt=1e-14)
+    s2 = spec_of((16, 8, 4, 3e-9, 2e-9, 1e-9), dt=3e-14, renorm_every=2)
+    m = O.random_unit_field(s1.n, MS, 51)
+    a, b = engine_sim(s1, 64), engine_sim(s2, 64)
+    a.set_m(m)
+    b.set_m(m)
+    a.step(5)
+    a.set_stepper(E.StepperConfig(dt=3e-14, renormalize_every=2))
+    a.set_time(0.0, 0)
+    a.set_m(m)
+    assert np.array_equal(a.step(9, return_all=True), b.step(9, return_all=True))
+    assert np.array_equal(a.get_m(), b.get_m())
+    with pytest.raises(ValueError, match="dt must be > 0"):
+        a.set_stepper(E.StepperConfig(dt=0.0))
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_f32_field_readouts(prec):
+    s = spec_of((33, 17, 5, 2e-9, 2e-9, 3e-9))
+    sim, ref, m = pair(s, prec, seed=52)
+    h64, h32 = sim.effective_field(), sim.effective_field(dtype=np.float32)
+    assert h32.dtype == np.float32 and np.array_equal(h32, h64.astype(np.float32))
+    assert np.array_equal(sim.demag_field(dtype=np.float32), sim.demag_field().astype(np.float32))
+
+
+def test_prepare_async_captures_the_timed_graphs():
+    s = spec_of((64, 32, 8, 2e-9, 2e-9, 2e-9))
+    a, b = engine_sim(s, 32), engine_sim(s, 32)
+    m = O.random_unit_field(s.n, MS, 53)
+    a.set_m(m)
+    b.set_m(m)
+    launches = a.prepare_async(150)   # chunks of 64 + 64 + 22
+    assert launches >= 3 * 4
+    a.step_async(150)
+    a.sync()
+    b.step(150)
+    assert np.array_equal(a.get_m(), b.get_m())

@@ -113,8 +113,8 @@ def test_c4_xy_passes_512x512x4(prec):
               f"K5 k_c2r_x_llg_v<{t},512,SUMS=0,RS=0,FWD=0,MULTI=0>"]
     if prec == 32:
         expect += ["K2 k_fft_y_fwd_tma<f32,1024,FY=1>", "K4 k_fft_y_inv_tma<f32,1024,FY=1>"]
-    else:
-        expect += ["K2 k_fft_y_fwd<f64,1024,FY=1>", "K4 k_fft_y_inv<f64,1024,FY=1>"]
+    else:   # three-stage plan
+        expect += ["K2 k_fft_y_fwd_tma<f64,1024,FY=1>", "K4 k_fft_y_inv_tma<f64,1024,FY=1>"]
     run_case(bench_spec(512, 512, 4), prec, expect, env={"MFD_FUSE_K1": "0"}, steps=12)
 
 
@@ -133,7 +133,7 @@ def test_sp4_refined_c2_f64():
 
 
 def test_cube_c3_f32():
-    """C3 128^3: K3 at Pz=256 (16 columns, 128-register budget), fused K1 at N=128."""
+    """C3 128^3: K3 at Pz=256 (radix 32 x 8, 16 columns), fused K1 at N=128."""
     run_case(bench_spec(128, 128, 128), 32, [
         "K1 k_r2c_x<f32,128,RS=0,MULTI=0>",
         "K3 k_fft_z_conv2<f32,256,FZ=1,SROW=1>",
