@@ -236,6 +236,8 @@ void Engine<T>::init() {
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_);
             small_x_ = L >= 2 && L <= kSmallXMax && k5_blocks_ < 2 * nsm && g.nx % V16<T>::V == 0;
+            if (const char* e = getenv("MFD_SMALL_X"))   // A/B switch: 0 off, 1 on where the variants exist
+                small_x_ = L >= 2 && L <= kSmallXMax && g.nx % V16<T>::V == 0 && atoi(e) != 0;
             if (small_x_) k5_blocks_ = nrows;
             // L2 prefetch distances: one resident wave of CTAs
             int per1 = 0, per5 = 0;

@@ -76,14 +76,24 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 #ifndef MFD_K3_F64_KPRE
 #define MFD_K3_F64_KPRE 1   // f64 K3: tensor bins one register phase ahead
 #endif
+#ifndef MFD_K5_F64_T1
+// f64 K5 sized for one first-stage FFT task per thread: ROWS = max(1, 512/N) rows,
+// NT = 3 ROWS N / R0 threads (96 at N = 512) at 5 CTAs/SM (128 registers, no spill).
+// C4 f64 K5 0.837 -> 0.725 ms against 2 rows x 256 threads at 2 CTAs/SM, where a
+// quarter of the threads idled through every FFT stage.  0: the 2 x 256 layout
+#define MFD_K5_F64_T1 1
+#endif
 template <class T, int N, int RS = 0> struct LCfg {   // K5
+    static constexpr bool T1 = sizeof(T) == 8 && RS == 0 && MFD_K5_F64_T1 && N >= 64 && Plan<T, N>::S >= 2;
     static constexpr int ROWS = RS > 0 ? RS
+                                : T1   ? cmax(1, 512 / N)
                                        : (sizeof(T) == 8 && MFD_K5_F64_ROWS > 0 ? cmin(MFD_K5_F64_ROWS, cmax(1, cmin(32, 2048 / cmax(N, 1))))
                                                                                : cmax(1, cmin(32, 2048 / cmax(N, 1))));
-    static constexpr int NT = RS > 0 ? 64 : 256;
+    static constexpr int NT = RS > 0 ? 64 : T1 ? clampNT(3 * ROWS * N / Plan<T, N>::R0) : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
     static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
-                                               : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
+                                : T1       ? cmax(1, cmin(cmin(5, 65536 / (NT * 128)), (220 * 1024) / SMEM))
+                                           : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
 };
 // dynamic shared memory of a K5 variant
 template <class T, int N, int RS, bool FWD> constexpr int k5_smem() { return LCfg<T, N, RS>::SMEM; }
@@ -371,8 +381,17 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
 #ifndef MFD_K2_TMA3
 #define MFD_K2_TMA3 1   // TMA-staged K2 also for three-stage plans (f32 Py = 2048, f64 Py = 1024)
 #endif
+#ifndef MFD_K2_T3_ROWB
+// three-stage TMA K2: 128-byte tile rows where work + staging fit 220 KB (f64 Py = 1024:
+// 0.610 -> 0.589 ms against the plain K2's 64-byte rows); 0: the plain K2's rows
+#define MFD_K2_T3_ROWB 128
+#endif
 template <class T, int L> struct YTCfg {
-    static constexpr int W = YCfg<T, L>::W, NT = YCfg<T, L>::NT, CS = sizeof(C2<T>);
+    static constexpr int CS = sizeof(C2<T>);
+    static constexpr bool WIDE = Plan<T, L>::S == 3 && MFD_K2_T3_ROWB > 0 &&
+                                 (MFD_K2_T3_ROWB / CS) * L * CS * 3 / 2 + 128 <= 220 * 1024;
+    static constexpr int W = WIDE ? MFD_K2_T3_ROWB / CS : YCfg<T, L>::W;
+    static constexpr int NT = clampNT(W * L / regE<T>());
     static constexpr int SMEM = W * L * CS + W * (L / 2) * CS + 128;   // work + staging (ny <= L/2 rows) + align
     static constexpr int MINB = 2 * SMEM <= 220 * 1024 ? 2 : 1;
     // Measured (f32): Py = 1024 0.317 -> 0.243 ms (512x512x64); at Py = 256 the

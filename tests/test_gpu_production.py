@@ -129,7 +129,9 @@ def test_sp4_refined_c2_f32():
 def test_sp4_refined_c2_f64():
     s = bench_spec(512, 128, 4, Ku=0.0, h_ext=(-19576.1, 3421.8, 0.0), dt=4e-15)
     s.dx, s.dy, s.dz = 500e-9 / 512, 125e-9 / 128, 0.75e-9
-    run_case(s, 64, ["K1 k_r2c_x<f64,512,RS=2,MULTI=0>"], steps=10)
+    # f64 K5 runs one row per CTA at N = 512, so 512 rows fill the SMs without the 1-2-row variants
+    run_case(s, 64, ["K1 k_r2c_x<f64,512,RS=0,MULTI=0>", "K5 k_c2r_x_llg_v<f64,512,SUMS=0,RS=0,FWD=1,MULTI=0>"],
+             steps=10)
 
 
 def test_cube_c3_f32():
