@@ -83,16 +83,27 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 // quarter of the threads idled through every FFT stage.  0: the 2 x 256 layout
 #define MFD_K5_F64_T1 1
 #endif
+#ifndef MFD_K5_F32_T1
+#define MFD_K5_F32_T1 0        // the same layout for f32 K5 (A/B switch)
+#endif
+#ifndef MFD_K5_F32_T1_ROWS
+#define MFD_K5_F32_T1_ROWS 4   // f32 T1: rows per CTA at N = 512
+#endif
+#ifndef MFD_K5_F32_T1_REGS
+#define MFD_K5_F32_T1_REGS 80  // f32 T1: register budget per thread
+#endif
 template <class T, int N, int RS = 0> struct LCfg {   // K5
-    static constexpr bool T1 = sizeof(T) == 8 && RS == 0 && MFD_K5_F64_T1 && N >= 64 && Plan<T, N>::S >= 2;
+    static constexpr bool T1 = RS == 0 && (sizeof(T) == 8 ? MFD_K5_F64_T1 : MFD_K5_F32_T1) && N >= 64 &&
+                               Plan<T, N>::S >= 2;
+    static constexpr int T1REGS = sizeof(T) == 8 ? 128 : MFD_K5_F32_T1_REGS;
     static constexpr int ROWS = RS > 0 ? RS
-                                : T1   ? cmax(1, 512 / N)
+                                : T1   ? cmax(1, (sizeof(T) == 8 ? 1 : MFD_K5_F32_T1_ROWS) * 512 / N)
                                        : (sizeof(T) == 8 && MFD_K5_F64_ROWS > 0 ? cmin(MFD_K5_F64_ROWS, cmax(1, cmin(32, 2048 / cmax(N, 1))))
                                                                                : cmax(1, cmin(32, 2048 / cmax(N, 1))));
     static constexpr int NT = RS > 0 ? 64 : T1 ? clampNT(3 * ROWS * N / Plan<T, N>::R0) : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
-    static constexpr int MINB = sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
-                                : T1       ? cmax(1, cmin(cmin(5, 65536 / (NT * 128)), (220 * 1024) / SMEM))
+    static constexpr int MINB = T1 ? cmax(1, cmin(cmin(sizeof(T) == 8 ? 5 : 8, 65536 / (NT * T1REGS)), (220 * 1024) / SMEM))
+                                : sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
                                            : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
 };
 // dynamic shared memory of a K5 variant
@@ -298,11 +309,16 @@ __device__ __forceinline__ void k1_body(const Geo& g, const T* __restrict__ M, C
     }
 }
 
+#ifndef MFD_K1_F64_MINB
+#define MFD_K1_F64_MINB 0   // f64 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
+#endif
 #ifndef MFD_K1_MINB
 #define MFD_K1_MINB 0   // f32 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
 #endif
 template <class T, int N, int RS = 0, bool MULTI = false>
-__global__ void __launch_bounds__(XCfg<T, N, RS>::NT, (sizeof(T) == 4 && RS == 0 && MFD_K1_MINB > 0) ? MFD_K1_MINB : 1)
+__global__ void __launch_bounds__(XCfg<T, N, RS>::NT, (sizeof(T) == 4 && RS == 0 && MFD_K1_MINB > 0)   ? MFD_K1_MINB
+                                                       : (sizeof(T) == 8 && RS == 0 && MFD_K1_F64_MINB > 0) ? MFD_K1_F64_MINB
+                                                                                                           : 1)
 k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __restrict__ tw, Ctl ctl) {
     if (halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
