@@ -83,6 +83,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 // quarter of the threads idled through every FFT stage.  0: the 2 x 256 layout
 #define MFD_K5_F64_T1 1
 #endif
+#ifndef MFD_K5_RS_NT
+#define MFD_K5_RS_NT 64   // threads of the 1-2-row K5 variants (small grids)
+#endif
 #ifndef MFD_K5_F32_T1
 #define MFD_K5_F32_T1 0        // the same layout for f32 K5 (A/B switch)
 #endif
@@ -100,7 +103,7 @@ template <class T, int N, int RS = 0> struct LCfg {   // K5
                                 : T1   ? cmax(1, (sizeof(T) == 8 ? 1 : MFD_K5_F32_T1_ROWS) * 512 / N)
                                        : (sizeof(T) == 8 && MFD_K5_F64_ROWS > 0 ? cmin(MFD_K5_F64_ROWS, cmax(1, cmin(32, 2048 / cmax(N, 1))))
                                                                                : cmax(1, cmin(32, 2048 / cmax(N, 1))));
-    static constexpr int NT = RS > 0 ? 64 : T1 ? clampNT(3 * ROWS * N / Plan<T, N>::R0) : 256;
+    static constexpr int NT = RS > 0 ? MFD_K5_RS_NT : T1 ? clampNT(3 * ROWS * N / Plan<T, N>::R0) : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
     static constexpr int MINB = T1 ? cmax(1, cmin(cmin(sizeof(T) == 8 ? 5 : 8, 65536 / (NT * T1REGS)), (220 * 1024) / SMEM))
                                 : sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
@@ -981,12 +984,17 @@ k_fft_z_conv1(Geo g, C2<T>* __restrict__ B, const T* __restrict__ Kt, const int*
 // in registers (one thread per (y frequency, x bin), as k_fft_z_conv1) and
 // the inverse y FFT (shared -> A), so the three passes cost one launch and no
 // B round trip.  Arithmetic per column is the same as K2 / K3 / K4.
+#ifndef MFD_YZ_W
+// y-z small pass: x bins per CTA (upper bound).  One bin per 32-thread CTA (129 CTAs at
+// SP4) instead of 4 per 128 threads: SP4 0.0114 -> 0.0106 ms/step
+#define MFD_YZ_W 1
+#endif
 template <class T, int LY, int LZ> struct YZCfg {
     static constexpr int CS = sizeof(C2<T>);
     static constexpr int NZH = LZ / 2 > 0 ? LZ / 2 : 1;               // z planes held (nz <= LZ/2)
-    static constexpr int W = cmax(1, cmin(4, 4096 / (3 * NZH * LY)));  // x bins per CTA
+    static constexpr int W = cmax(1, cmin(MFD_YZ_W, 4096 / (3 * NZH * LY)));  // x bins per CTA
     static constexpr int NCOL = 3 * NZH * W;                            // columns (comp, z, bin)
-    static constexpr int NT = 128;
+    static constexpr int NT = MFD_YZ_W == 4 ? 128 : 32 * MFD_YZ_W;
     static constexpr int SMEM = NCOL * LY * CS;
     // Measured (f32): SP4 128x32x1 0.0164 -> 0.0107 ms/step; at 512x128x4 (W = 1)
     // the per-CTA work is too thin and the separate passes win (0.040 vs 0.057 ms)
@@ -1014,10 +1022,10 @@ __device__ __forceinline__ void yz_body(const Geo& g, C2<T>* __restrict__ A, con
     };
     auto lds = [&](int col, int pos) -> C2<T> { return sm[pos * NCOL + col]; };
     auto sts = [&](int col, int pos, C2<T> v) { sm[pos * NCOL + col] = v; };
+    const int Hz = LZ / 2 + 1;
     fft_forward<T, LY, NCOL, NT, true, false, true>(ld0, lds, sts, sts, tw);
     __syncthreads();
     // z: one item per (y frequency v, bin w); frequencies in natural order
-    const int Hz = LZ / 2 + 1;
     for (int e = threadIdx.x; e < LY * W; e += NT) {
         const int w = e % W, v = e / W;
         const int pos = ybuf[v];
