@@ -83,6 +83,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 // quarter of the threads idled through every FFT stage.  0: the 2 x 256 layout
 #define MFD_K5_F64_T1 1
 #endif
+#ifndef MFD_K5_DEFER_HALT
+#define MFD_K5_DEFER_HALT 1   // 1-2-row K5 variants: halt flag checked at the first barrier (A/B switch)
+#endif
 #ifndef MFD_K5_RS_NT
 #define MFD_K5_RS_NT 64   // threads of the 1-2-row K5 variants (small grids)
 #endif
@@ -215,6 +218,21 @@ __device__ __forceinline__ bool halted(const Ctl& c) {
         if (sqrt(r) / c.Ms * c.rad2deg <= c.tol) return true;
     }
     return false;
+}
+// The same test split in two: the raw loads (issued early, nothing waits on
+// them) and the decision (taken where the values are needed).
+struct HaltRaw {
+    int err;
+    unsigned long long tq;
+};
+__device__ __forceinline__ HaltRaw halted_load(const Ctl& c) {
+    HaltRaw h;
+    h.err = *(volatile int*)c.err;
+    h.tq = c.prev_torque ? *(volatile unsigned long long*)c.prev_torque : 0ull;
+    return h;
+}
+__device__ __forceinline__ int halted_test(const Ctl& c, const HaltRaw& h) {
+    return h.err != 0 || (c.prev_torque && sqrt(__longlong_as_double((long long)h.tq)) / c.Ms * c.rad2deg <= c.tol);
 }
 
 // Real-to-complex post-process of one pair (k, N-k) of a row whose N-point
@@ -1556,7 +1574,8 @@ template <class T, int N, bool SUMS, int RS = 0, bool FWD = false, bool MULTI = 
 __device__ __forceinline__ void k5_body(const Geo& g, C2<T>* __restrict__ A, const T* __restrict__ M,
                                         T* __restrict__ Mn, T* __restrict__ Hout, const C2<T>* __restrict__ tw,
                                         T scale, const LocalParams<T>& P, const StepIO& io, const Halo<T>& hl,
-                                        long long bx, unsigned char* smem_raw, double& tmax, double* acc, int& bad) {
+                                        long long bx, unsigned char* smem_raw, double& tmax, double* acc, int& bad,
+                                        const Ctl* hctl = nullptr, HaltRaw hold = {}) {
     constexpr bool fwd = FWD;
     using CF = LCfg<T, N, RS>;
     constexpr int ROWS = CF::ROWS, NT = CF::NT, LP = xpitch<T, N>(), NCOL = 3 * ROWS;
@@ -1631,7 +1650,11 @@ __device__ __forceinline__ void k5_body(const Geo& g, C2<T>* __restrict__ A, con
             if (k == 0 && N > 1) pre(sm + col * LP, N / 2, pc[it], pc[it]);
         }
     }
-    __syncthreads();
+    // hold: the caller's deferred halt-flag read (nothing global is written before this barrier)
+    if (__syncthreads_or(hctl ? halted_test(*hctl, hold) : 0)) {
+        bad = -1;
+        return;
+    }
     if constexpr (Plan<T, N>::S > 0) {
         auto lds = [&](int col, int pos) -> C2<T> { return sm[col * LP + xpad<T>(pos)]; };
         auto sts = [&](int col, int pos, C2<T> v) { sm[col * LP + xpad<T>(pos)] = v; };
@@ -1686,12 +1709,18 @@ __global__ void __launch_bounds__(LCfg<T, N, RS>::NT, LCfg<T, N, RS>::MINB)
 k_c2r_x_llg_v(Geo g, C2<T>* __restrict__ A, const T* __restrict__ M, T* __restrict__ Mn,
               T* __restrict__ Hout, const C2<T>* __restrict__ tw, T scale, LocalParams<T> P, StepIO io, Ctl ctl,
               Halo<T> hl) {
-    if (halted(ctl)) return;
+    // small grids (latency-bound): the halt flag loads alongside the spectrum rows
+    // and is acted on at k5_body's first barrier, before any global write
+    constexpr bool DEFER = RS > 0 && MFD_K5_DEFER_HALT;
+    if (!DEFER && halted(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double tmax = 0;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
     int bad = 0;
-    k5_body<T, N, SUMS, RS, FWD, MULTI>(g, A, M, Mn, Hout, tw, scale, P, io, hl, blockIdx.x, smem_raw, tmax, acc, bad);
+    const HaltRaw hr = DEFER ? halted_load(ctl) : HaltRaw{};
+    k5_body<T, N, SUMS, RS, FWD, MULTI>(g, A, M, Mn, Hout, tw, scale, P, io, hl, blockIdx.x, smem_raw, tmax, acc, bad,
+                                        DEFER ? &ctl : nullptr, hr);
+    if (DEFER && bad < 0) return;
     block_finish<LCfg<T, N, RS>::NT>(io, ctl, tmax, acc, bad);
 }
 
