@@ -83,6 +83,9 @@ template <class T, int N, int RS = 0> struct XCfg {   // K1
 // quarter of the threads idled through every FFT stage.  0: the 2 x 256 layout
 #define MFD_K5_F64_T1 1
 #endif
+#ifndef MFD_K5_F32_MINB
+#define MFD_K5_F32_MINB 3   // f32 K5 (RS = 0): resident CTAs/SM its register budget assumes
+#endif
 #ifndef MFD_K5_DEFER_HALT
 #define MFD_K5_DEFER_HALT 1   // 1-2-row K5 variants: halt flag checked at the first barrier (A/B switch)
 #endif
@@ -109,7 +112,7 @@ template <class T, int N, int RS = 0> struct LCfg {   // K5
     static constexpr int NT = RS > 0 ? MFD_K5_RS_NT : T1 ? clampNT(3 * ROWS * N / Plan<T, N>::R0) : 256;
     static constexpr int SMEM = 3 * ROWS * xpitch<T, N>() * (int)sizeof(C2<T>);
     static constexpr int MINB = T1 ? cmax(1, cmin(cmin(sizeof(T) == 8 ? 5 : 8, 65536 / (NT * T1REGS)), (220 * 1024) / SMEM))
-                                : sizeof(T) == 4 ? cmax(1, cmin(3, (200 * 1024) / SMEM))
+                                : sizeof(T) == 4 ? cmax(1, cmin(MFD_K5_F32_MINB, (200 * 1024) / SMEM))
                                            : (MFD_K5_F64_MINB > 1 && MFD_K5_F64_MINB * SMEM <= 226 * 1024 ? MFD_K5_F64_MINB : 1);
 };
 // dynamic shared memory of a K5 variant
@@ -334,7 +337,10 @@ __device__ __forceinline__ void k1_body(const Geo& g, const T* __restrict__ M, C
 #define MFD_K1_F64_MINB 0   // f64 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
 #endif
 #ifndef MFD_K1_MINB
-#define MFD_K1_MINB 0   // f32 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
+// f32 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained, 141
+// registers at N = 512, 3 CTAs/SM).  4 (128 registers, no spill): C4 K1 0.160 -> 0.142 ms,
+// C5 1.271 -> 1.122 ms; 5 (96 registers) spills at N = 1024; 6-7 spill everywhere
+#define MFD_K1_MINB 4
 #endif
 template <class T, int N, int RS = 0, bool MULTI = false>
 __global__ void __launch_bounds__(XCfg<T, N, RS>::NT, (sizeof(T) == 4 && RS == 0 && MFD_K1_MINB > 0)   ? MFD_K1_MINB
