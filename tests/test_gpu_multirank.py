@@ -26,7 +26,10 @@ def make(g, prec, world, **kw):
                         world=world, virtual_ranks=world > 1)
 
 
-GRIDS = [(16, 12, 8, 2e-9, 2e-9, 2e-9), (33, 17, 4, 2e-9, 3e-9, 2e-9), (64, 32, 16, 2e-9, 2e-9, 2e-9)]
+GRIDS = [(16, 12, 8, 2e-9, 2e-9, 2e-9), (33, 17, 4, 2e-9, 3e-9, 2e-9), (64, 32, 16, 2e-9, 2e-9, 2e-9),
+         (4, 512, 4, 1e-9, 1e-9, 1e-9),     # Py = 1024: two-stage TMA y passes (f32), three-stage (f64)
+         (4, 1024, 4, 1e-9, 1e-9, 1e-9),    # Py = 2048: three-stage TMA y passes
+         (4, 4, 128, 2e-9, 2e-9, 1e-9)]     # Pz = 256: K3 radix 32 x 8
 
 
 @pytest.mark.parametrize("prec", [64, 32])
