@@ -34,6 +34,7 @@ SIZE_GRIDS = [
     (64, 48, 40, 2e-9, 2e-9, 2e-9), (200, 100, 3, 2e-9, 2e-9, 2e-9),
     (20, 12, 100, 2e-9, 2e-9, 1e-9),                # Pz = 256 with nz < Pz/2 (K3 non-FZ, radix 32 x 8)
     (3, 768, 1, 1e-9, 1e-9, 1e-9),                  # Py = 2048 with ny < Py/2 (three-stage TMA K2, FY=0)
+    (6, 200, 2, 1e-9, 1e-9, 1e-9),                  # Py = 512: TMA y passes, three-stage in f64
 ]
 
 
