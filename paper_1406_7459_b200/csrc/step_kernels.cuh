@@ -354,7 +354,7 @@ k_r2c_x(Geo g, const T* __restrict__ M, C2<T>* __restrict__ A, const C2<T>* __re
 
 // Measured on B200 (512x512x64 f32): the swizzle removes the conflicts but the
 // extra integer work made K2 slower (0.32 -> 0.40 ms), so it is off.
-constexpr bool kYSwizzle = false;
+constexpr bool kYSwizzle = false;   // re-measured with the TMA K2: 0.238 -> 0.242 ms (C4), C5 +0.6 %
 // y-pass shared tile [pos][W]: with 64-byte position rows, the last stage's
 // tasks (stride R_last positions apart) would land two per bank group; XOR the
 // row parity with the stride bit so a half-warp covers both 64-byte halves.
@@ -449,7 +449,9 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
                 const C2<T>* __restrict__ tw, Ctl ctl, int ntx, int box_rows, int comp0, int ncomp) {
     using CF = YTCfg<T, L>;
     constexpr int W = CF::W, NT = CF::NT;
-    constexpr int TWL = kK2StridedTw ? TWN : L;
+    // dense L-entry twiddle table for two-stage plans (C4 f32: K2 0.238 -> 0.233 ms), the
+    // TWN-strided copy for three-stage ones (C5: 2.32 vs 2.37 ms with the dense table)
+    constexpr int TWL = kK2StridedTw && Plan<T, L>::S == 3 ? TWN : L;
     // no halt check: K2-K4 touch only spectrum scratch (see Ctl)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2<T>* work = reinterpret_cast<C2<T>*>(smem_raw);
