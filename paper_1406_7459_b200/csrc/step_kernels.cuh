@@ -421,6 +421,9 @@ k_fft_y_fwd(Geo g, const C2<T>* __restrict__ A, C2<T>* __restrict__ B, const C2<
 // buffer (cp.async.bulk.tensor, mbarrier-completed) while the current tile runs
 // its second FFT stage, so no warp waits on global loads.  Same arithmetic as
 // k_fft_y_fwd.
+#ifndef MFD_K2_REV
+#define MFD_K2_REV 1   // TMA K2 tiles in reverse order (C5 K2 2.32 -> 2.27 ms; C4 neutral)
+#endif
 #ifndef MFD_K2_TMA3
 #define MFD_K2_TMA3 1   // TMA-staged K2 also for three-stage plans (f32 Py = 2048, f64 Py = 1024)
 #endif
@@ -468,7 +471,11 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
         tma_prefetch_desc(&tmA);
     }
     __syncthreads();
-    auto issue = [&](int tt) {   // one thread
+    // MFD_K2_REV: tiles in reverse order, so the first ones read the A rows K1 wrote
+    // last (still in L2)
+    auto tmap = [&](int tt) { return MFD_K2_REV ? ntiles - 1 - tt : tt; };
+    auto issue = [&](int t0) {   // one thread
+        const int tt = tmap(t0);
         const int bx = tt % ntx, k = (tt / ntx) % nz, comp = comp0 + tt / (ntx * nz);
         const int kb = k / g.nz, kl = k - kb * g.nz;   // plane k came from rank kb
         const int row0 = ((kb * 3 + comp) * g.nz + kl) * ny;
@@ -486,7 +493,8 @@ k_fft_y_fwd_tma(Geo g, const __grid_constant__ CUtensorMap tmA, C2<T>* __restric
     };
 #pragma unroll 1
     for (; t < ntiles; t += gridDim.x) {
-        const int bx = t % ntx, k = (t / ntx) % nz, comp = comp0 + t / (ntx * nz);
+        const int tt = tmap(t);
+        const int bx = tt % ntx, k = (tt / ntx) % nz, comp = comp0 + tt / (ntx * nz);
         const int u0 = bx * W;
         C2<T>* dst = B + comp * g.S_c + k * g.S_k + u0;
         auto stn = [&](int col, int pos, C2<T> v) { dst[pos * Wb + col] = v; };
