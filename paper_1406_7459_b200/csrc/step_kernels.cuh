@@ -334,7 +334,9 @@ __device__ __forceinline__ void k1_body(const Geo& g, const T* __restrict__ M, C
 }
 
 #ifndef MFD_K1_F64_MINB
-#define MFD_K1_F64_MINB 0   // f64 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained)
+// f64 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained, 92
+// registers, 5 CTAs/SM).  4 (128 registers): C4 f64 K1 0.347 -> 0.335 ms; 6 spills
+#define MFD_K1_F64_MINB 4
 #endif
 #ifndef MFD_K1_MINB
 // f32 K1 (RS = 0): resident CTAs/SM its register budget assumes (0: unconstrained, 141
